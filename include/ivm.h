@@ -1,0 +1,154 @@
+/*
+ * ivm.h -- C ABI of the B200-native certified interval-FFT multiplier.
+ *
+ * The operation is the paper's "rigorous extension of the Schoenhage-Strassen
+ * algorithm" (arXiv 1006.0405, /root/reference/PAPER.md, cited P:<line>):
+ *   input  x, y in Z_b^n, b = 256,
+ *   output z in Z_b^{2n} with z = x*y,
+ * computed as: zero-pad to m = 2^k, k = ceil(log2(2n-1)),
+ * forward FFT of both, pointwise product,
+ * inverse FFT, all on rectangular complex interval
+ * containment sets with directed rounding; then each coefficient
+ * interval must contain exactly one integer -- "choose the unique integer in
+ * the containment set ... if [it] contains multiple integers, then we report
+ * an error" -- and the certified coefficients are carried back to
+ * base 256.  A product is returned only when certified; an
+ * uncertified pair is not an error of the call: its flag is 0 and its digits
+ * are zero ("increase the precision ... or use a different algorithm").
+ *
+ * Conventions for every entry point:
+ *   - digits are base 256, little-endian (digit i has weight 256^i), uint8;
+ *     both operands have the same length n >= 1 (the caller zero-pads the
+ *     shorter one); the product has exactly 2n digits (z_{2n-1} is the final
+ *     carry) and is not canonicalised;
+ *   - batched arrays are row-major: a, b = [batch][n], prod = [batch][2n],
+ *     certified = [batch] (1 = certified, 0 = needs more precision);
+ *   - pointers passed to ivm_multiply* are DEVICE pointers on the context's
+ *     device; the caller allocates and owns them (the context owns only its
+ *     twiddle tables and scratch);
+ *   - calls are asynchronous on `cuda_stream` (a cudaStream_t, NULL = legacy
+ *     default stream); outputs are valid after the stream is synchronised;
+ *   - precision: IVM_F64 = binary64 intervals (P:5), IVM_F32 = binary32
+ *     (P:22);
+ *   - errors: argument errors (n == 0, batch == 0, NULL required pointer,
+ *     unknown precision, n beyond the supported maximum) return before any
+ *     launch and write nothing; CUDA failures return IVM_ECUDA and are
+ *     sticky for the context;
+ *   - determinism: identical inputs give bitwise identical outputs;
+ *   - thread safety: one host thread per context at a time.
+ */
+#ifndef IVM_H
+#define IVM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ivm_ctx *ivm_ctx_t;
+
+enum { IVM_F64 = 0, IVM_F32 = 1 };
+
+enum {
+    IVM_OK = 0,
+    IVM_EINVAL = -1,        /* bad argument */
+    IVM_ENOMEM = -2,        /* device or host allocation failed */
+    IVM_ECUDA = -3,         /* CUDA runtime / launch error (sticky) */
+    IVM_EUNSUPPORTED = -4,  /* size / precision not supported by this build */
+    IVM_ENODEV = -6         /* no CUDA device */
+};
+
+/* Version string of the library ("ivm <semver> sm_100a"). */
+const char *ivm_version(void);
+
+/* Human-readable text of a status code. */
+const char *ivm_strerror(int status);
+
+/* Largest supported operand length n for a precision (0 if none). */
+size_t ivm_max_digits(int prec);
+
+/* FFT length m = 2^ceil(log2(2n-1)) used for operands of n digits. */
+size_t ivm_fft_length(size_t n);
+
+/* Create a context on CUDA device `device` (selects it on the calling
+ * thread).  *ctx is set on success. */
+int ivm_create(ivm_ctx_t *ctx, int device);
+
+/* Destroy a context; frees tables and scratch.  NULL is a no-op. */
+int ivm_destroy(ivm_ctx_t ctx);
+
+/* Optional: build the twiddle table for (n, prec) and size the scratch for
+ * `batch` so that the first multiply does no allocation. */
+int ivm_reserve(ivm_ctx_t ctx, size_t n, size_t batch, int prec);
+
+/* One multiplication (the paper's problem):
+ * a, b: [n] device digits; prod: [2n] device digits; certified: 1 device byte. */
+int ivm_multiply(ivm_ctx_t ctx, const uint8_t *a, const uint8_t *b, size_t n,
+                 uint8_t *prod, uint8_t *certified, int prec, void *cuda_stream);
+
+/* Batched independent multiplications: a, b [batch][n], prod [batch][2n],
+ * certified [batch] (all device pointers). */
+int ivm_multiply_batched(ivm_ctx_t ctx, const uint8_t *a, const uint8_t *b, size_t n,
+                         size_t batch, uint8_t *prod, uint8_t *certified, int prec,
+                         void *cuda_stream);
+
+/* Diagnostics for parity tests; every output is nullable (device pointers):
+ *   max_radius [batch]   : max over coefficients i < 2n-1 of (hi-lo)/2 of the
+ *                          real and imaginary parts (binary64, rounded up);
+ *   first_bad  [batch]   : smallest i < 2n-1 whose interval does not certify,
+ *                          -1 if certified;
+ *   coeffs [batch][2n-1] : the snapped integer coefficients c_i (valid where
+ *                          the pair is certified);
+ *   dump_pairs [n_dump]  : pair indices whose final coefficient intervals are
+ *                          written to intervals [n_dump][m][4] as binary64
+ *                          (re.lo, re.hi, im.lo, im.hi), m = ivm_fft_length(n). */
+int ivm_multiply_batched_diag(ivm_ctx_t ctx, const uint8_t *a, const uint8_t *b, size_t n,
+                              size_t batch, uint8_t *prod, uint8_t *certified, int prec,
+                              void *cuda_stream, double *max_radius, int32_t *first_bad,
+                              int64_t *coeffs, const int32_t *dump_pairs, size_t n_dump,
+                              double *intervals);
+
+/* Host-pointer convenience (end-to-end path): copies a, b (host, [batch][n])
+ * to the device, multiplies, and copies prod / certified back to host
+ * buffers, all on `cuda_stream`; returns after the stream is synchronised.
+ * Uses context-owned device staging buffers. */
+int ivm_multiply_batched_host(ivm_ctx_t ctx, const uint8_t *a, const uint8_t *b, size_t n,
+                              size_t batch, uint8_t *prod, uint8_t *certified, int prec,
+                              void *cuda_stream);
+
+/* Seeded synthetic digits on the device (the counter-based SplitMix64
+ * generator of SURVEY.md §8(d.2); same bits as
+ * paper_1006_0405_b200/inputs.py).  kind: 0 uniform, 1 all-255, 2 sparse
+ * (90 % zeros), 3 uniform with nonzero most significant digit; kinds: NULL
+ * (use `kind` for all pairs) or [batch] device bytes.  Writes [batch][n]
+ * digits of operand `operand` (0 = a, 1 = b) for pairs pair0 .. pair0+batch-1. */
+int ivm_generate_digits(ivm_ctx_t ctx, uint8_t *out, size_t n, size_t batch, uint64_t seed,
+                        uint64_t pair0, int operand, int kind, const uint8_t *kinds,
+                        void *cuda_stream);
+
+/* Directed-rounding FP64 / FP32 throughput probe: runs `iters` dependent
+ * chains of DFMA.RP / FFMA.RP on every SM; writes the number of executed
+ * FMA instructions (thread level) to *fma_count (host).  The caller times
+ * the call with events on `cuda_stream`.  sink: device buffer of
+ * >= 148*1024 doubles. */
+int ivm_peak_probe(ivm_ctx_t ctx, int prec, int iters, double *sink, uint64_t *fma_count,
+                   void *cuda_stream);
+
+/* Number of kernels launched by the last ivm_multiply* call on this context. */
+int ivm_last_launch_count(ivm_ctx_t ctx);
+
+/* Host-side copy of the twiddle table the kernels use for m = 2^log2m:
+ * out = [m][4] (re.lo, re.hi, im.lo, im.hi) of omega_m^j = e^{2 pi i j/m}
+ * (P:68), the optimal enclosures [RD, RU] of cos and sin; out is double[m][4]
+ * for IVM_F64 and float[m][4] for IVM_F32 (host memory, caller-owned).
+ * Returns IVM_EUNSUPPORTED if an entry cannot be rounded rigorously.
+ * Needs no device. */
+int ivm_twiddle_table(int log2m, int prec, void *out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* IVM_H */

@@ -1,0 +1,206 @@
+"""B200-native certified interval-FFT multiplication (arXiv 1006.0405).
+
+Thin ctypes binding over ``libivm.so`` (include/ivm.h).  Argument marshalling
+only: every step of the multiply runs in the library's sm_100a kernels.
+PyTorch provides device memory and streams.  There is no CPU fallback: if the
+library is missing or no device is present the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+__all__ = ["lib", "Context", "IvmError", "F64", "F32", "fft_length", "max_digits",
+           "twiddle_table", "EXPORTS"]
+
+F64, F32 = 0, 1
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libivm.so")
+
+# every symbol include/ivm.h declares
+EXPORTS = ["ivm_version", "ivm_strerror", "ivm_max_digits", "ivm_fft_length", "ivm_create",
+           "ivm_destroy", "ivm_reserve", "ivm_multiply", "ivm_multiply_batched",
+           "ivm_multiply_batched_diag", "ivm_multiply_batched_host", "ivm_generate_digits",
+           "ivm_peak_probe", "ivm_last_launch_count", "ivm_twiddle_table"]
+
+
+class IvmError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        msg = lib().ivm_strerror(status).decode() if _lib is not None else str(status)
+        super().__init__(f"{what}: {msg} ({status})")
+        self.status = status
+
+
+_lib = None
+
+
+def lib():
+    """Load libivm.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_1006_0405_b200.build` "
+                              "(there is no fallback implementation)")
+        L = ctypes.CDLL(LIB_PATH)
+        P, S, I, U64 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_uint64
+        L.ivm_version.restype = ctypes.c_char_p
+        L.ivm_strerror.restype = ctypes.c_char_p
+        L.ivm_strerror.argtypes = [I]
+        L.ivm_max_digits.restype = S
+        L.ivm_max_digits.argtypes = [I]
+        L.ivm_fft_length.restype = S
+        L.ivm_fft_length.argtypes = [S]
+        L.ivm_create.argtypes = [ctypes.POINTER(P), I]
+        L.ivm_destroy.argtypes = [P]
+        L.ivm_reserve.argtypes = [P, S, S, I]
+        L.ivm_multiply.argtypes = [P, P, P, S, P, P, I, P]
+        L.ivm_multiply_batched.argtypes = [P, P, P, S, S, P, P, I, P]
+        L.ivm_multiply_batched_diag.argtypes = [P, P, P, S, S, P, P, I, P, P, P, P, P, S, P]
+        L.ivm_multiply_batched_host.argtypes = [P, P, P, S, S, P, P, I, P]
+        L.ivm_generate_digits.argtypes = [P, P, S, S, U64, U64, I, I, P, P]
+        L.ivm_peak_probe.argtypes = [P, I, I, P, ctypes.POINTER(U64), P]
+        L.ivm_last_launch_count.argtypes = [P]
+        L.ivm_twiddle_table.argtypes = [I, I, P]
+        _lib = L
+    return _lib
+
+
+def _check(status: int, what: str):
+    if status != 0:
+        raise IvmError(status, what)
+
+
+def fft_length(n: int) -> int:
+    return int(lib().ivm_fft_length(n))
+
+
+def max_digits(prec: int = F64) -> int:
+    return int(lib().ivm_max_digits(prec))
+
+
+def twiddle_table(log2m: int, prec: int = F64):
+    """The library's optimal twiddle enclosures, [m][4] (host, numpy)."""
+    import numpy as np
+    m = 1 << log2m
+    out = np.zeros((m, 4), np.float64 if prec == F64 else np.float32)
+    _check(lib().ivm_twiddle_table(log2m, prec, out.ctypes.data), "ivm_twiddle_table")
+    return out
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+class Context:
+    """One device context (twiddle tables + scratch).  Tensors are torch CUDA
+    tensors on the context's device; results are valid after the stream syncs."""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        h = ctypes.c_void_p()
+        _check(lib().ivm_create(ctypes.byref(h), device), "ivm_create")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().ivm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def reserve(self, n: int, batch: int, prec: int = F64):
+        _check(lib().ivm_reserve(self._h, n, batch, prec), "ivm_reserve")
+
+    @property
+    def last_launch_count(self) -> int:
+        return int(lib().ivm_last_launch_count(self._h))
+
+    def multiply(self, a, b, prec: int = F64, out=None, cert=None, stream=None):
+        """Batched multiply of uint8 CUDA tensors a, b [batch][n] (or [n])."""
+        import torch
+        squeeze = a.dim() == 1
+        if squeeze:
+            a, b = a[None], b[None]
+        assert a.dtype == torch.uint8 and b.dtype == torch.uint8 and a.shape == b.shape
+        assert a.is_cuda and b.is_cuda and a.is_contiguous() and b.is_contiguous()
+        B, n = a.shape
+        if out is None:
+            out = torch.empty((B, 2 * n), dtype=torch.uint8, device=a.device)
+        if cert is None:
+            cert = torch.empty((B,), dtype=torch.uint8, device=a.device)
+        _check(lib().ivm_multiply_batched(self._h, _ptr(a), _ptr(b), n, B, _ptr(out), _ptr(cert),
+                                          prec, _stream(stream)), "ivm_multiply_batched")
+        if squeeze:
+            return out[0], cert[0]
+        return out, cert
+
+    def multiply_diag(self, a, b, prec: int = F64, dump_pairs=None, stream=None, coeffs=True):
+        """Multiply with diagnostics: returns dict of CUDA tensors."""
+        import torch
+        B, n = a.shape
+        dev = a.device
+        m = fft_length(n)
+        out = torch.empty((B, 2 * n), dtype=torch.uint8, device=dev)
+        cert = torch.empty((B,), dtype=torch.uint8, device=dev)
+        rad = torch.empty((B,), dtype=torch.float64, device=dev)
+        bad = torch.empty((B,), dtype=torch.int32, device=dev)
+        co = torch.empty((B, 2 * n - 1), dtype=torch.int64, device=dev) if coeffs else None
+        dp, iv, nd = None, None, 0
+        if dump_pairs is not None and len(dump_pairs):
+            dp = torch.as_tensor(list(dump_pairs), dtype=torch.int32, device=dev)
+            nd = dp.numel()
+            iv = torch.empty((nd, m, 4), dtype=torch.float64, device=dev)
+        _check(lib().ivm_multiply_batched_diag(self._h, _ptr(a), _ptr(b), n, B, _ptr(out),
+                                               _ptr(cert), prec, _stream(stream), _ptr(rad),
+                                               _ptr(bad), _ptr(co), _ptr(dp), nd, _ptr(iv)),
+               "ivm_multiply_batched_diag")
+        return {"prod": out, "cert": cert, "max_radius": rad, "first_bad": bad, "coeffs": co,
+                "intervals": iv, "m": m}
+
+    def multiply_host(self, a, b, prec: int = F64, out=None, cert=None, stream=None):
+        """End-to-end path: host (pinned) uint8 tensors in, host tensors out."""
+        import torch
+        B, n = a.shape
+        if out is None:
+            out = torch.empty((B, 2 * n), dtype=torch.uint8, pin_memory=True)
+        if cert is None:
+            cert = torch.empty((B,), dtype=torch.uint8, pin_memory=True)
+        _check(lib().ivm_multiply_batched_host(self._h, _ptr(a), _ptr(b), n, B, _ptr(out),
+                                               _ptr(cert), prec, _stream(stream)),
+               "ivm_multiply_batched_host")
+        return out, cert
+
+    def generate_digits(self, n: int, batch: int, seed: int, operand: int, kind=0, pair0: int = 0,
+                        out=None, stream=None):
+        """Seeded digits on the device (same bits as inputs.py).  kind: int or
+        uint8 CUDA tensor of per-pair kinds."""
+        import torch
+        if out is None:
+            out = torch.empty((batch, n), dtype=torch.uint8, device=f"cuda:{self.device}")
+        kinds = None
+        k = 0
+        if isinstance(kind, int):
+            k = kind
+        else:
+            kinds = kind
+        _check(lib().ivm_generate_digits(self._h, _ptr(out), n, batch, seed & (2**64 - 1), pair0,
+                                         operand, k, _ptr(kinds), _stream(stream)),
+               "ivm_generate_digits")
+        return out
+
+    def peak_probe(self, prec: int, iters: int, sink, stream=None) -> int:
+        cnt = ctypes.c_uint64()
+        _check(lib().ivm_peak_probe(self._h, prec, iters, _ptr(sink), ctypes.byref(cnt),
+                                    _stream(stream)), "ivm_peak_probe")
+        return int(cnt.value)

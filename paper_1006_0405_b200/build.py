@@ -1,0 +1,72 @@
+"""Build libivm.so (sm_100a SASS, static cudart) in-tree.
+
+    python -m paper_1006_0405_b200.build          # incremental
+    python -m paper_1006_0405_b200.build --force  # rebuild everything
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+ROOT = os.path.dirname(HERE)
+OUT = os.path.join(HERE, "libivm.so")
+OBJ = os.path.join(HERE, "_obj")
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--ftz=false",
+                  "--prec-div=true", "--prec-sqrt=true", "--fmad=true", "-Xptxas", "-v",
+                  "-I", os.path.join(ROOT, "include")]
+CXXFLAGS = ["-O2", "-fPIC", "-std=gnu++17", "-fext-numeric-literals", "-I", os.path.join(ROOT, "include")]
+
+CU = ["ivm_kernels.cu", "ivm_api.cu"]
+CPP = ["ivm_planner.cpp"]
+HDR = ["ivm_interval.cuh", "ivm_fft.cuh", "ivm_internal.h"]
+
+
+def _stale(obj: str, src: str) -> bool:
+    if not os.path.exists(obj):
+        return True
+    t = os.path.getmtime(obj)
+    deps = [src] + [os.path.join(CSRC, h) for h in HDR] + [os.path.join(ROOT, "include", "ivm.h")]
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    os.makedirs(OBJ, exist_ok=True)
+    objs = []
+    for f in CU:
+        src, obj = os.path.join(CSRC, f), os.path.join(OBJ, f + ".o")
+        if force or _stale(obj, src):
+            cmd = [NVCC, *NVFLAGS, "-c", src, "-o", obj]
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            if r.returncode != 0:
+                sys.stderr.write(r.stdout + r.stderr)
+                raise RuntimeError(f"nvcc failed on {f}")
+            with open(obj + ".ptxas.txt", "w") as fh:
+                fh.write(r.stderr)
+            if verbose:
+                sys.stderr.write(r.stderr)
+        objs.append(obj)
+    for f in CPP:
+        src, obj = os.path.join(CSRC, f), os.path.join(OBJ, f + ".o")
+        if force or _stale(obj, src):
+            subprocess.check_call(["g++", *CXXFLAGS, "-c", src, "-o", obj])
+        objs.append(obj)
+    if force or not os.path.exists(OUT) or any(os.path.getmtime(o) > os.path.getmtime(OUT) for o in objs):
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", OUT, *objs,
+               "-Xlinker", "-Bstatic", "-lquadmath", "-Xlinker", "-Bdynamic", "-lrt", "-lpthread", "-ldl"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            # fall back to a dynamic libquadmath
+            cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", OUT, *objs, "-lquadmath"]
+            subprocess.check_call(cmd)
+    return OUT
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(OUT)

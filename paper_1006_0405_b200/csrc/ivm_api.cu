@@ -1,0 +1,299 @@
+// ivm_api.cu -- the C ABI (include/ivm.h): context, plan cache, launches.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <map>
+#include <mutex>
+#include <utility>
+#include <vector>
+
+#include "../../include/ivm.h"
+
+#include "ivm_internal.h"
+
+static const int kMaxLog2M = 13;  // CTA-resident path
+
+struct ivm_ctx {
+  int device = 0;
+  int sms = 0;
+  int sticky = 0;
+  bool consts = false;
+  std::map<std::pair<int, int>, void *> tw;  // (log2m, prec) -> device table
+  std::map<std::pair<int, int>, ivm::LaunchInfo> info;
+  void *ascratch = nullptr;
+  size_t ascratch_bytes = 0;
+  int32_t *slot = nullptr;
+  size_t slot_cap = 0;
+  uint8_t *stage = nullptr;  // host API staging: a | b | prod | cert
+  size_t stage_bytes = 0;
+  int last_launches = 0;
+};
+
+static int cuda_fail(ivm_ctx_t c) {
+  if (c) c->sticky = IVM_ECUDA;
+  return IVM_ECUDA;
+}
+
+static int log2m_for(size_t n) {
+  if (n <= 1) return 0;
+  size_t N = 1;
+  int m = 0;
+  while (N < 2 * n - 1) {
+    N <<= 1;
+    m++;
+  }
+  return m;
+}
+
+extern "C" {
+
+const char *ivm_version(void) { return "ivm 0.1.0 sm_100a"; }
+
+const char *ivm_strerror(int s) {
+  switch (s) {
+    case IVM_OK: return "ok";
+    case IVM_EINVAL: return "invalid argument";
+    case IVM_ENOMEM: return "out of memory";
+    case IVM_ECUDA: return "CUDA error";
+    case IVM_EUNSUPPORTED: return "unsupported size or precision";
+    case IVM_ENODEV: return "no CUDA device";
+    default: return "unknown status";
+  }
+}
+
+size_t ivm_max_digits(int prec) {
+  if (prec != IVM_F64 && prec != IVM_F32) return 0;
+  return ((size_t)1 << kMaxLog2M) / 2;  // 2n-1 <= 2^13
+}
+
+size_t ivm_fft_length(size_t n) { return n == 0 ? 0 : (size_t)1 << log2m_for(n); }
+
+int ivm_twiddle_table(int log2m, int prec, void *out) {
+  if (!out || log2m < 0 || log2m > 24 || (prec != IVM_F64 && prec != IVM_F32)) return IVM_EINVAL;
+  return ivm::plan_twiddles(log2m, prec, out) == 0 ? IVM_OK : IVM_EUNSUPPORTED;
+}
+
+int ivm_create(ivm_ctx_t *ctx, int device) {
+  if (!ctx) return IVM_EINVAL;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return IVM_ENODEV;
+  if (device < 0 || device >= ndev) return IVM_EINVAL;
+  if (cudaSetDevice(device) != cudaSuccess) return IVM_ECUDA;
+  ivm_ctx *c = new ivm_ctx();
+  c->device = device;
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+  double w64[32 * 4];
+  float w32[32 * 4];
+  if (ivm::plan_twiddles(5, 0, w64) != 0 || ivm::plan_twiddles(5, 1, w32) != 0) {
+    delete c;
+    return IVM_EUNSUPPORTED;
+  }
+  if (ivm::upload_w32(w64, w32) != 0) {
+    delete c;
+    return IVM_ECUDA;
+  }
+  c->consts = true;
+  *ctx = c;
+  return IVM_OK;
+}
+
+int ivm_destroy(ivm_ctx_t c) {
+  if (!c) return IVM_OK;
+  cudaSetDevice(c->device);
+  for (auto &kv : c->tw) cudaFree(kv.second);
+  cudaFree(c->ascratch);
+  cudaFree(c->slot);
+  cudaFree(c->stage);
+  delete c;
+  return IVM_OK;
+}
+
+static int get_table(ivm_ctx_t c, int m, int prec, const void **out) {
+  auto key = std::make_pair(m, prec);
+  auto it = c->tw.find(key);
+  if (it != c->tw.end()) {
+    *out = it->second;
+    return IVM_OK;
+  }
+  const size_t N = (size_t)1 << m, es = prec == IVM_F64 ? 8 : 4;
+  std::vector<unsigned char> h(N * 4 * es);
+  if (ivm::plan_twiddles(m, prec, h.data()) != 0) return IVM_EUNSUPPORTED;
+  void *d = nullptr;
+  if (cudaMalloc(&d, h.size()) != cudaSuccess) return IVM_ENOMEM;
+  if (cudaMemcpy(d, h.data(), h.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(d);
+    return cuda_fail(c);
+  }
+  c->tw[key] = d;
+  *out = d;
+  return IVM_OK;
+}
+
+static int get_info(ivm_ctx_t c, int m, int prec, ivm::LaunchInfo *li) {
+  auto key = std::make_pair(m, prec);
+  auto it = c->info.find(key);
+  if (it != c->info.end()) {
+    *li = it->second;
+    return IVM_OK;
+  }
+  int r = ivm::cta_info(prec, m, li);
+  if (r == -4) return IVM_EUNSUPPORTED;
+  if (r != 0 || li->blocks_per_sm < 1) return cuda_fail(c);
+  c->info[key] = *li;
+  return IVM_OK;
+}
+
+static int grid_for(ivm_ctx_t c, const ivm::LaunchInfo &li, size_t batch) {
+  size_t g = (size_t)c->sms * (size_t)li.blocks_per_sm;
+  if (g > batch) g = batch;
+  return (int)g;
+}
+
+static int ensure_scratch(ivm_ctx_t c, size_t bytes) {
+  if (bytes <= c->ascratch_bytes) return IVM_OK;
+  cudaFree(c->ascratch);
+  c->ascratch = nullptr;
+  c->ascratch_bytes = 0;
+  if (cudaMalloc(&c->ascratch, bytes) != cudaSuccess) return IVM_ENOMEM;
+  c->ascratch_bytes = bytes;
+  return IVM_OK;
+}
+
+static int check_args(ivm_ctx_t c, const void *a, const void *b, size_t n, size_t batch, const void *p,
+                      const void *cert, int prec) {
+  if (!c || !a || !b || !p || !cert || n == 0 || batch == 0) return IVM_EINVAL;
+  if (prec != IVM_F64 && prec != IVM_F32) return IVM_EINVAL;
+  if (n > ivm_max_digits(prec)) return IVM_EUNSUPPORTED;
+  if (batch > (size_t)0x7fffffff) return IVM_EINVAL;
+  if (c->sticky) return c->sticky;
+  return IVM_OK;
+}
+
+int ivm_reserve(ivm_ctx_t c, size_t n, size_t batch, int prec) {
+  if (!c || n == 0 || batch == 0 || (prec != IVM_F64 && prec != IVM_F32)) return IVM_EINVAL;
+  if (n > ivm_max_digits(prec)) return IVM_EUNSUPPORTED;
+  if (cudaSetDevice(c->device) != cudaSuccess) return cuda_fail(c);
+  int m = log2m_for(n);
+  if (m < 2) return IVM_OK;
+  const void *t;
+  int r = get_table(c, m, prec, &t);
+  if (r) return r;
+  ivm::LaunchInfo li;
+  r = get_info(c, m, prec, &li);
+  if (r) return r;
+  if (!li.a_smem) return ensure_scratch(c, (size_t)grid_for(c, li, batch) * li.a_bytes_per_cta);
+  return IVM_OK;
+}
+
+int ivm_multiply_batched_diag(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, size_t n, size_t batch,
+                              uint8_t *prod, uint8_t *cert, int prec, void *stream, double *max_radius,
+                              int32_t *first_bad, int64_t *coeffs, const int32_t *dump_pairs,
+                              size_t n_dump, double *intervals) {
+  int r = check_args(c, a, b, n, batch, prod, cert, prec);
+  if (r) return r;
+  if (n_dump && (!dump_pairs || !intervals)) return IVM_EINVAL;
+  if (cudaSetDevice(c->device) != cudaSuccess) return cuda_fail(c);
+  cudaStream_t s = (cudaStream_t)stream;
+  ivm::KParams kp{};
+  kp.a = a; kp.b = b; kp.prod = prod; kp.cert = cert;
+  kp.n = (int)n; kp.batch = (int)batch;
+  kp.max_radius = max_radius; kp.first_bad = first_bad; kp.coeffs = coeffs;
+  kp.intervals = intervals;
+  int launches = 0;
+  if (n_dump) {
+    if (c->slot_cap < batch) {
+      cudaFree(c->slot);
+      c->slot = nullptr;
+      c->slot_cap = 0;
+      if (cudaMalloc(&c->slot, batch * sizeof(int32_t)) != cudaSuccess) return IVM_ENOMEM;
+      c->slot_cap = batch;
+    }
+    if (ivm::dump_map_launch(c->slot, (int)batch, dump_pairs, (int)n_dump, s) != 0) return cuda_fail(c);
+    launches += 2;
+    kp.dump_slot = c->slot;
+  }
+  int m = log2m_for(n);
+  if (m == 0) {
+    if (ivm::n1_launch(kp, s) != 0) return cuda_fail(c);
+    c->last_launches = launches + 1;
+    return IVM_OK;
+  }
+  const void *tw;
+  r = get_table(c, m, prec, &tw);
+  if (r) return r;
+  ivm::LaunchInfo li;
+  r = get_info(c, m, prec, &li);
+  if (r) return r;
+  int grid = grid_for(c, li, batch);
+  if (!li.a_smem) {
+    r = ensure_scratch(c, (size_t)grid * li.a_bytes_per_cta);
+    if (r) return r;
+    kp.ascratch = c->ascratch;
+  }
+  kp.tw = tw;
+  if (ivm::cta_launch(prec, m, kp, grid, s) != 0) return cuda_fail(c);
+  c->last_launches = launches + 1;
+  return IVM_OK;
+}
+
+int ivm_multiply_batched(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, size_t n, size_t batch,
+                         uint8_t *prod, uint8_t *cert, int prec, void *stream) {
+  return ivm_multiply_batched_diag(c, a, b, n, batch, prod, cert, prec, stream, nullptr, nullptr,
+                                   nullptr, nullptr, 0, nullptr);
+}
+
+int ivm_multiply(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, size_t n, uint8_t *prod,
+                 uint8_t *cert, int prec, void *stream) {
+  return ivm_multiply_batched(c, a, b, n, 1, prod, cert, prec, stream);
+}
+
+int ivm_multiply_batched_host(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, size_t n, size_t batch,
+                              uint8_t *prod, uint8_t *cert, int prec, void *stream) {
+  int r = check_args(c, a, b, n, batch, prod, cert, prec);
+  if (r) return r;
+  if (cudaSetDevice(c->device) != cudaSuccess) return cuda_fail(c);
+  const size_t in = n * batch, out = 2 * n * batch;
+  const size_t need = 2 * in + out + batch;
+  if (c->stage_bytes < need) {
+    cudaFree(c->stage);
+    c->stage = nullptr;
+    c->stage_bytes = 0;
+    if (cudaMalloc(&c->stage, need) != cudaSuccess) return IVM_ENOMEM;
+    c->stage_bytes = need;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  uint8_t *da = c->stage, *db = da + in, *dp = db + in, *dc = dp + out;
+  if (cudaMemcpyAsync(da, a, in, cudaMemcpyHostToDevice, s) != cudaSuccess) return cuda_fail(c);
+  if (cudaMemcpyAsync(db, b, in, cudaMemcpyHostToDevice, s) != cudaSuccess) return cuda_fail(c);
+  r = ivm_multiply_batched(c, da, db, n, batch, dp, dc, prec, stream);
+  if (r) return r;
+  if (cudaMemcpyAsync(prod, dp, out, cudaMemcpyDeviceToHost, s) != cudaSuccess) return cuda_fail(c);
+  if (cudaMemcpyAsync(cert, dc, batch, cudaMemcpyDeviceToHost, s) != cudaSuccess) return cuda_fail(c);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_fail(c);
+  return IVM_OK;
+}
+
+int ivm_generate_digits(ivm_ctx_t c, uint8_t *out, size_t n, size_t batch, uint64_t seed, uint64_t pair0,
+                        int operand, int kind, const uint8_t *kinds, void *stream) {
+  if (!c || !out || n == 0 || batch == 0 || kind < 0 || kind > 3 || (operand != 0 && operand != 1))
+    return IVM_EINVAL;
+  if (n > 0x7fffffff) return IVM_EINVAL;
+  if (cudaSetDevice(c->device) != cudaSuccess) return cuda_fail(c);
+  if (ivm::digits_launch(out, (int)n, (long long)batch, seed, pair0, operand, kind, kinds, c->sms,
+                         (cudaStream_t)stream) != 0)
+    return cuda_fail(c);
+  return IVM_OK;
+}
+
+int ivm_peak_probe(ivm_ctx_t c, int prec, int iters, double *sink, uint64_t *count, void *stream) {
+  if (!c || !sink || !count || iters <= 0 || (prec != IVM_F64 && prec != IVM_F32)) return IVM_EINVAL;
+  if (cudaSetDevice(c->device) != cudaSuccess) return cuda_fail(c);
+  if (ivm::probe_launch(prec, iters, sink, c->sms, (cudaStream_t)stream, count) != 0) return cuda_fail(c);
+  return IVM_OK;
+}
+
+int ivm_last_launch_count(ivm_ctx_t c) { return c ? c->last_launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,40 @@
+// ivm_internal.h -- declarations shared by ivm_api.cu and ivm_kernels.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace ivm {
+
+struct KParams {
+  const uint8_t *a, *b;
+  uint8_t *prod, *cert;
+  int n, batch;
+  const void *tw;            // CI<T>[m]: omega_m^j
+  void *ascratch;            // [gridDim.x][2][m/2+1] split re/im when A is not in SMEM
+  double *max_radius;        // [batch] nullable
+  int32_t *first_bad;        // [batch] nullable
+  int64_t *coeffs;           // [batch][2n-1] nullable
+  const int32_t *dump_slot;  // [batch] slot or -1 (nullable)
+  double *intervals;         // [n_dump][m][4]
+};
+
+struct LaunchInfo {
+  int threads;
+  size_t smem;
+  bool a_smem;
+  size_t a_bytes_per_cta;
+  int blocks_per_sm;
+};
+
+int upload_w32(const double *w64, const float *w32);
+int cta_info(int prec, int m, LaunchInfo *li);
+int cta_launch(int prec, int m, const KParams &kp, int grid, cudaStream_t s);
+int n1_launch(const KParams &kp, cudaStream_t s);
+int digits_launch(uint8_t *out, int n, long long batch, uint64_t seed, uint64_t pair0, int operand,
+                  int kind, const uint8_t *kinds, int sms, cudaStream_t s);
+int probe_launch(int prec, int iters, void *sink, int sms, cudaStream_t s, uint64_t *count);
+int dump_map_launch(int32_t *slot, int batch, const int32_t *pairs, int n_dump, cudaStream_t s);
+int plan_twiddles(int m, int prec, void *out);
+
+}  // namespace ivm

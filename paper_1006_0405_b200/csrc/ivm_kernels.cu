@@ -1,0 +1,713 @@
+// ivm_kernels.cu -- sm_100a kernels of the certified interval-FFT multiplier.
+//
+// One CTA multiplies one pair at a time (persistent over the batch) with
+// everything on chip for m = 2^k <= 8192 (fp64) / 16384 (fp32):
+//
+//   fwd(a) : pass 0 reads the digits straight from HBM (P:208 zero-padding is
+//            a load guard), passes 1.. run in shared memory; a's half
+//            spectrum A[k], k <= m/2, is kept in SMEM or parked in L2/HBM
+//   fwd(b) : same, its last pass fused with the pointwise product
+//            and the first inverse pass in registers
+//   inv    : remaining inverse passes, then x 2^-k, round-and-certify
+//            (P:24), coefficient snap
+//   carry  : byte split + binary carry-lookahead (warp ballots)
+//
+// FFT schedule: Stockham-ordered decimation-in-time with radix-R register
+// passes; every butterfly is DIT form (twiddle on one input, then add/sub,
+// P:153).  The input is real and the output is real, so only half of each
+// intermediate spectrum is computed and stored (Hermitian symmetry of real
+// data: the other half is the exact conjugate); see DESIGN.md "FFT schedule"
+// and tools/proto_halfstock.py for the index rules.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ivm_fft.cuh"
+#include "ivm_internal.h"
+
+namespace ivm {
+
+// ---------------------------------------------------------------------------
+// compile-time plans
+// ---------------------------------------------------------------------------
+struct PlanT {
+  int nf, f[4];  // forward radices (f[0] reads digits; R=32 only there, pruned)
+  int ni, q[5];  // inverse radices (q[0] == f[nf-1]: fused with fwd(b) last)
+};
+
+__host__ __device__ constexpr PlanT plan_for(int m) {
+  switch (m) {
+    case 2: return PlanT{2, {2, 2, 0, 0}, 2, {2, 2, 0, 0, 0}};
+    case 3: return PlanT{2, {2, 4, 0, 0}, 2, {4, 2, 0, 0, 0}};
+    case 4: return PlanT{2, {4, 4, 0, 0}, 2, {4, 4, 0, 0, 0}};
+    case 5: return PlanT{2, {2, 16, 0, 0}, 2, {16, 2, 0, 0, 0}};
+    case 6: return PlanT{2, {4, 16, 0, 0}, 2, {16, 4, 0, 0, 0}};
+    case 7: return PlanT{2, {8, 16, 0, 0}, 2, {16, 8, 0, 0, 0}};
+    case 8: return PlanT{2, {16, 16, 0, 0}, 2, {16, 16, 0, 0, 0}};
+    case 9: return PlanT{2, {32, 16, 0, 0}, 3, {16, 4, 8, 0, 0}};
+    case 10: return PlanT{3, {4, 16, 16, 0}, 3, {16, 4, 16, 0, 0}};
+    case 11: return PlanT{3, {8, 16, 16, 0}, 3, {16, 8, 16, 0, 0}};
+    case 12: return PlanT{3, {16, 16, 16, 0}, 3, {16, 16, 16, 0, 0}};
+    case 13: return PlanT{3, {32, 16, 16, 0}, 4, {16, 4, 8, 16, 0}};
+    case 14: return PlanT{4, {4, 16, 16, 16}, 4, {16, 4, 16, 16, 0}};
+    default: return PlanT{0, {0, 0, 0, 0}, 0, {0, 0, 0, 0, 0}};
+  }
+}
+
+__host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
+__host__ __device__ constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
+__host__ __device__ constexpr int gper(int R) { return R >= 16 ? 1 : 16 / R; }  // tasks/thread
+
+// forward L_p (product of the first p radices)
+__host__ __device__ constexpr int fwdL(const PlanT &P, int p) {
+  return p == 0 ? 1 : fwdL(P, p - 1) * P.f[p - 1];
+}
+__host__ __device__ constexpr int invL(const PlanT &P, int p) {
+  return p == 0 ? 1 : invL(P, p - 1) * P.q[p - 1];
+}
+
+template <int M> struct Geo {
+  static constexpr PlanT P = plan_for(M);
+  static constexpr int N = 1 << M;
+  static constexpr int threads_needed() {
+    int t = 32;
+    for (int p = 1; p < P.nf; p++) {  // forward in-place passes and fused pass
+      int L = fwdL(P, p), R = P.f[p], Sp = N / L / R;
+      int cnt = (L / 2 + 1) * Sp;
+      t = cmax(t, cdiv(cnt, gper(R)));
+    }
+    for (int p = 1; p + 1 < P.ni; p++) {  // inverse in-place passes
+      int L = invL(P, p), Q = P.q[p], Sp = N / L / Q;
+      int cnt = L * (Sp / 2 + 1);
+      t = cmax(t, cdiv(cnt, gper(Q)));
+    }
+    return cdiv(t, 32) * 32;
+  }
+  static constexpr int cap() {  // state capacity (elements)
+    int c = 0;
+    for (int p = 1; p < P.nf; p++) c = cmax(c, (fwdL(P, p) / 2 + 1) * (N / fwdL(P, p)));
+    for (int p = 1; p < P.ni; p++) c = cmax(c, invL(P, p) * (N / invL(P, p) / 2 + 1));
+    return c;
+  }
+  static constexpr int THREADS = threads_needed();
+  static constexpr int CAP = cap();
+  static constexpr int AH = N / 2 + 1;  // stored half spectrum of a
+};
+
+template <typename T> struct V2;
+template <> struct V2<double> { using t = double2; };
+template <> struct V2<float> { using t = float2; };
+
+template <typename T> struct Arr {  // split (re, im) interval array
+  typename V2<T>::t *re, *im;
+  __device__ __forceinline__ CI<T> ld(int i) const {
+    auto r = re[i], m = im[i];
+    return CI<T>{r.x, r.y, m.x, m.y};
+  }
+  __device__ __forceinline__ void st(int i, const CI<T> &z) const {
+    re[i] = typename V2<T>::t{z.rl, z.rh};
+    im[i] = typename V2<T>::t{z.il, z.ih};
+  }
+};
+
+template <typename T>
+__device__ __forceinline__ CI<T> ldtw(const CI<T> *__restrict__ tw, int m) {
+  const typename V2<T>::t *p = reinterpret_cast<const typename V2<T>::t *>(tw) + 2 * m;
+  auto r = __ldg(p), i = __ldg(p + 1);
+  return CI<T>{r.x, r.y, i.x, i.y};
+}
+
+// ---------------------------------------------------------------------------
+// forward pass 0: digits (real, punctual, zero-padded) -> F_1[r][v], r <= R/2
+// ---------------------------------------------------------------------------
+template <typename T, int N, int R>
+__device__ void fwd_pass0(const uint8_t *__restrict__ dig, int n, Arr<T> st) {
+  constexpr int S1 = N / R;
+  for (int v = threadIdx.x; v < S1; v += blockDim.x) {
+    if constexpr (R == 32) {
+      // x_q = 0 for q >= 16 (index >= m/2 >= n): X[2s] = DFT16(x)[s],
+      // X[2s+1] = DFT16(x_q w_32^q)[s]
+      T xd[16];
+#pragma unroll
+      for (int q = 0; q < 16; q++) {
+        int idx = v + S1 * q;
+        xd[q] = idx < n ? T(dig[idx]) : T(0);
+      }
+      CI<T> y[16];
+#pragma unroll
+      for (int q = 0; q < 16; q++) y[q] = punctual(xd[q]);
+      dft<T, 16, false>(y);
+#pragma unroll
+      for (int s = 0; s <= 8; s++) st.st((2 * s) * S1 + v, y[s]);
+#pragma unroll
+      for (int q = 0; q < 16; q++) y[q] = q == 0 ? punctual(xd[0]) : twmul(cw32<T>(q), punctual(xd[q]));
+      dft<T, 16, false>(y);
+#pragma unroll
+      for (int s = 0; s < 8; s++) st.st((2 * s + 1) * S1 + v, y[s]);
+    } else {
+      CI<T> x[R];
+#pragma unroll
+      for (int q = 0; q < R; q++) {
+        int idx = v + S1 * q;
+        x[q] = punctual(idx < n ? T(dig[idx]) : T(0));
+      }
+      dft<T, R, false>(x);
+#pragma unroll
+      for (int r = 0; r <= R / 2; r++) st.st(r * S1 + v, x[r]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// forward pass p >= 1: F_p[k0][v + S'q] -> F_{p+1}, k0 <= L/2 (half storage)
+// dst may alias src (in place: all loads before the barrier, then stores)
+// ---------------------------------------------------------------------------
+template <typename T, int N, int R, int L>
+__device__ void fwd_mid(Arr<T> src, Arr<T> dst, const CI<T> *__restrict__ tw) {
+  constexpr int S = N / L, Sp = S / R, COUNT = (L / 2 + 1) * Sp, G = gper(R);
+  CI<T> v[G][R];
+  int k0s[G], nus[G];
+#pragma unroll
+  for (int g = 0; g < G; g++) {
+    int t = threadIdx.x + g * blockDim.x;
+    k0s[g] = t / Sp;
+    nus[g] = t % Sp;
+    if (t < COUNT) {
+      const int k0 = k0s[g], nu = nus[g];
+#pragma unroll
+      for (int q = 0; q < R; q++) {
+        CI<T> z = src.ld(k0 * S + nu + Sp * q);
+        if (q > 0 && k0 != 0) z = twmul(ldtw(tw, (q * k0 * Sp) & (N - 1)), z);
+        v[g][q] = z;
+      }
+      dft<T, R, false>(v[g]);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int g = 0; g < G; g++) {
+    int t = threadIdx.x + g * blockDim.x;
+    if (t < COUNT) {
+      const int k0 = k0s[g], nu = nus[g];
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        const int kap = k0 + L * r;
+        if (k0 == 0) {
+          if (2 * r <= R) dst.st(kap * Sp + nu, v[g][r]);
+        } else if (2 * k0 == L) {
+          if (2 * r < R) dst.st(kap * Sp + nu, v[g][r]);
+        } else if (2 * kap <= L * R) {
+          dst.st(kap * Sp + nu, v[g][r]);
+        } else {
+          dst.st((L * R - kap) * Sp + nu, cconj(v[g][r]));
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fwd(b) last pass + pointwise product + inverse pass 0
+//   k0 in [0, L/2]: X_B[k0 + L r] (r < R) in registers; A from its store;
+//   P = A * X_B; E_1[r'][k0] = sum_r wbar_R^{r r'} P_r
+// ---------------------------------------------------------------------------
+template <typename T, int N, int R, int L>
+__device__ void fwd_last_fused(Arr<T> st, Arr<T> A, const CI<T> *__restrict__ tw) {
+  static_assert(L * R == N, "last pass");
+  constexpr int COUNT = L / 2 + 1, G = gper(R), H1 = L / 2 + 1;
+  CI<T> v[G][R];
+#pragma unroll
+  for (int g = 0; g < G; g++) {
+    const int k0 = threadIdx.x + g * blockDim.x;
+    if (k0 < COUNT) {
+#pragma unroll
+      for (int q = 0; q < R; q++) {
+        CI<T> z = st.ld(k0 * R + q);
+        if (q > 0 && k0 != 0) z = twmul(ldtw(tw, (q * k0) & (N - 1)), z);
+        v[g][q] = z;
+      }
+      dft<T, R, false>(v[g]);
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        const int idx = k0 + L * r;
+        CI<T> a = (2 * idx <= N) ? A.ld(idx) : cconj(A.ld(N - idx));
+        v[g][r] = cmul(a, v[g][r]);
+      }
+      dft<T, R, true>(v[g]);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int g = 0; g < G; g++) {
+    const int k0 = threadIdx.x + g * blockDim.x;
+    if (k0 < COUNT) {
+#pragma unroll
+      for (int r = 0; r < R; r++) st.st(r * H1 + k0, v[g][r]);
+    }
+  }
+}
+
+// inverse input load with the Hermitian mirror:
+//   E_p[k0][mu] stored for mu <= S/2; E_p[k][S-v] = w_L^k conj(E_p[k][v]);
+//   twiddled value wbar_{LQ}^{q k0} E_p[k0][mu]
+template <typename T, int N, int Q, int L>
+__device__ __forceinline__ CI<T> inv_load(Arr<T> st, const CI<T> *__restrict__ tw, int k0, int mu,
+                                          int q) {
+  constexpr int S = N / L, Sp = S / Q, H = S / 2 + 1;
+  if (2 * mu <= S) {
+    CI<T> z = st.ld(k0 * H + mu);
+    if (q > 0 && k0 != 0) z = twmul(cconj(ldtw(tw, (q * k0 * Sp) & (N - 1))), z);
+    return z;
+  } else {
+    CI<T> z = cconj(st.ld(k0 * H + S - mu));
+    if (k0 != 0) z = twmul(ldtw(tw, ((Q - q) * k0 * Sp) & (N - 1)), z);
+    return z;
+  }
+}
+
+template <typename T, int N, int Q, int L>
+__device__ void inv_mid(Arr<T> st, const CI<T> *__restrict__ tw) {
+  constexpr int S = N / L, Sp = S / Q, Hn = Sp / 2 + 1, COUNT = L * Hn, G = gper(Q);
+  CI<T> v[G][Q];
+  int k0s[G], nus[G];
+#pragma unroll
+  for (int g = 0; g < G; g++) {
+    int t = threadIdx.x + g * blockDim.x;
+    k0s[g] = t / Hn;
+    nus[g] = t % Hn;
+    if (t < COUNT) {
+#pragma unroll
+      for (int q = 0; q < Q; q++) v[g][q] = inv_load<T, N, Q, L>(st, tw, k0s[g], nus[g] + Sp * q, q);
+      dft<T, Q, true>(v[g]);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int g = 0; g < G; g++) {
+    int t = threadIdx.x + g * blockDim.x;
+    if (t < COUNT) {
+#pragma unroll
+      for (int r = 0; r < Q; r++) st.st((k0s[g] + L * r) * Hn + nus[g], v[g][r]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// round-and-certify
+// ---------------------------------------------------------------------------
+struct CertShared {
+  int ok;
+  int first_bad;
+  unsigned long long maxrad_bits;  // non-negative doubles order like integers
+  unsigned warp_g, warp_p;          // carry scan
+  unsigned warp_cin;
+};
+
+template <typename T>
+__device__ __forceinline__ void certify_one(const CI<T> &z, int i, int n, int32_t *coef,
+                                           CertShared &cs, double *dump) {
+  if (dump) {
+    double4 d = make_double4((double)z.rl, (double)z.rh, (double)z.il, (double)z.ih);
+    reinterpret_cast<double4 *>(dump)[i] = d;
+  }
+  if (i >= 2 * n - 1) return;
+  const double rl = (double)z.rl, rh = (double)z.rh, il = (double)z.il, ih = (double)z.ih;
+  const double cl = ceil(rl), fh = floor(rh);
+  const bool ok = (cl == fh) && (ceil(il) == 0.0) && (floor(ih) == 0.0);
+  const double rad = fmax(__dmul_ru(__dadd_ru(rh, -rl), 0.5), __dmul_ru(__dadd_ru(ih, -il), 0.5));
+  if (!(rad <= 1e300)) {  // NaN / inf
+    atomicMax(&cs.maxrad_bits, (unsigned long long)__double_as_longlong(__longlong_as_double(0x7ff0000000000000ULL)));
+  } else {
+    atomicMax(&cs.maxrad_bits, (unsigned long long)__double_as_longlong(rad));
+  }
+  if (ok) {
+    coef[i] = (int32_t)cl;
+  } else {
+    cs.ok = 0;
+    atomicMin(&cs.first_bad, i);
+    coef[i] = 0;
+  }
+}
+
+template <typename T, int N, int Q, int L>
+__device__ void inv_last(Arr<T> st, const CI<T> *__restrict__ tw, int n, int32_t *coef,
+                         CertShared &cs, double *dump) {
+  static_assert(L * Q == N, "inverse last pass");
+  constexpr int H = Q / 2 + 1;
+  const T scale = T(1) / T(N);  // 2^-k, exact
+  for (int k0 = threadIdx.x; k0 < L; k0 += blockDim.x) {
+    CI<T> v[Q];
+#pragma unroll
+    for (int q = 0; q < Q; q++) {
+      if (2 * q <= Q) {
+        CI<T> z = st.ld(k0 * H + q);
+        if (q > 0 && k0 != 0) z = twmul(cconj(ldtw(tw, (q * k0) & (N - 1))), z);
+        v[q] = z;
+      } else {
+        CI<T> z = cconj(st.ld(k0 * H + Q - q));
+        if (k0 != 0) z = twmul(ldtw(tw, ((Q - q) * k0) & (N - 1)), z);
+        v[q] = z;
+      }
+    }
+    dft<T, Q, true>(v);
+#pragma unroll
+    for (int r = 0; r < Q; r++) {
+      CI<T> z = v[r];
+      z.rl = DR<T>::mul_rd(z.rl, scale);
+      z.rh = DR<T>::mul_ru(z.rh, scale);
+      z.il = DR<T>::mul_rd(z.il, scale);
+      z.ih = DR<T>::mul_ru(z.ih, scale);
+      certify_one(z, k0 + L * r, n, coef, cs, dump);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// carry: c_i < 2^31 split into bytes; t_i = sum_b byte_b(c_{i-b})
+// <= 1020; u_i = (t_i & 255) + (t_{i-1} >> 8) <= 258; then binary carries
+// with generate u >= 256 / propagate u == 255 (carry-lookahead by ballots).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int coef_at(const int32_t *coef, int i, int nc) {
+  return (i >= 0 && i < nc) ? coef[i] : 0;
+}
+__device__ __forceinline__ int t_at(const int32_t *coef, int i, int nc) {
+  int t = 0;
+#pragma unroll
+  for (int b = 0; b < 4; b++) t += (coef_at(coef, i - b, nc) >> (8 * b)) & 255;
+  return t;
+}
+__device__ __forceinline__ int u_at(const int32_t *coef, int i, int nc) {
+  return (t_at(coef, i, nc) & 255) + (t_at(coef, i - 1, nc) >> 8);
+}
+
+__device__ void carry_store(const int32_t *coef, int n, uint8_t *__restrict__ out, bool certified,
+                            CertShared &cs) {
+  const int nout = 2 * n;
+  if (!certified) {
+    for (int i = threadIdx.x; i < nout; i += blockDim.x) out[i] = 0;
+    return;
+  }
+  const int nc = 2 * n - 1, npos = 2 * n + 4;
+  const int T = blockDim.x, K = (npos + T - 1) / T;
+  const int p0 = threadIdx.x * K, p1 = min(p0 + K, npos);
+  // chunk generate / propagate
+  int c = 0;
+  bool allp = true;
+  for (int i = p0; i < p1; i++) {
+    int u = u_at(coef, i, nc);
+    allp = allp && (u == 255);
+    c = (u + c) >> 8;
+  }
+  const bool G = c != 0, Pp = allp;
+  const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = (T + 31) >> 5;
+  const unsigned g = __ballot_sync(0xffffffffu, G), p = __ballot_sync(0xffffffffu, Pp);
+  __shared__ unsigned wg[32], wp[32], wc[32];
+  if (lane == 0) {
+    unsigned long long s = (unsigned long long)(g | p) + g;
+    wg[warp] = (unsigned)(s >> 32);
+    wp[warp] = (p == 0xffffffffu);
+  }
+  __syncthreads();
+  if (warp == 0) {
+    bool gg = lane < nwarps ? wg[lane] != 0 : false;
+    bool pp = lane < nwarps ? wp[lane] != 0 : true;
+    unsigned G2 = __ballot_sync(0xffffffffu, gg), P2 = __ballot_sync(0xffffffffu, pp);
+    unsigned cin = ((G2 | P2) + G2) ^ P2;
+    if (lane < nwarps) wc[lane] = (cin >> lane) & 1u;
+  }
+  __syncthreads();
+  const unsigned c0 = wc[warp];
+  const unsigned long long s = (unsigned long long)(g | p) + g + c0;
+  const unsigned cin_vec = (unsigned)s ^ p;
+  int cc = (cin_vec >> lane) & 1u;
+  for (int i = p0; i < p1; i++) {
+    int u = u_at(coef, i, nc) + cc;
+    if (i < nout) out[i] = (uint8_t)(u & 255);
+    cc = u >> 8;
+  }
+  (void)cs;
+}
+
+// ---------------------------------------------------------------------------
+// the fused CTA kernel
+// ---------------------------------------------------------------------------
+
+template <typename T, int M> struct Cfg {
+  using G = Geo<M>;
+  static constexpr int N = G::N, THREADS = G::THREADS, CAP = G::CAP, AH = G::AH;
+  static constexpr size_t E = sizeof(typename V2<T>::t);
+  static constexpr size_t STATE_BYTES = 2 * E * (size_t)CAP;
+  static constexpr size_t A_BYTES = 2 * E * (size_t)AH;
+  static constexpr size_t COEF_BYTES = 4 * (size_t)N;
+  static constexpr bool A_SMEM = STATE_BYTES + A_BYTES + COEF_BYTES + 256 <= 110 * 1024;
+  static constexpr size_t SMEM = STATE_BYTES + (A_SMEM ? A_BYTES : 0) + COEF_BYTES;
+};
+
+template <typename T, int M, int F, int P>
+__device__ __forceinline__ void run_fwd_mids(Arr<T> st, Arr<T> A, const CI<T> *tw, bool is_a) {
+  // forward passes p = F .. nf-2 in place, and the last pass of a into A
+  constexpr PlanT PL = plan_for(M);
+  constexpr int N = 1 << M;
+  if constexpr (F < PL.nf - 1) {
+    fwd_mid<T, N, PL.f[F], fwdL(PL, F)>(st, st, tw);
+    __syncthreads();
+    run_fwd_mids<T, M, F + 1, P>(st, A, tw, is_a);
+  }
+}
+
+template <typename T, int M, int Pi>
+__device__ __forceinline__ void run_inv_mids(Arr<T> st, const CI<T> *tw) {
+  constexpr PlanT PL = plan_for(M);
+  constexpr int N = 1 << M;
+  if constexpr (Pi < PL.ni - 1) {
+    inv_mid<T, N, PL.q[Pi], invL(PL, Pi)>(st, tw);
+    __syncthreads();
+    run_inv_mids<T, M, Pi + 1>(st, tw);
+  }
+}
+
+template <typename T, int M>
+__global__ void __launch_bounds__(Cfg<T, M>::THREADS, 1) ivm_cta_kernel(KParams kp) {
+  using C = Cfg<T, M>;
+  constexpr PlanT PL = plan_for(M);
+  constexpr int N = C::N;
+  using V = typename V2<T>::t;
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ CertShared cs;
+  Arr<T> st{reinterpret_cast<V *>(smem), reinterpret_cast<V *>(smem) + C::CAP};
+  Arr<T> A;
+  int32_t *coef;
+  if constexpr (C::A_SMEM) {
+    A.re = reinterpret_cast<V *>(smem) + 2 * C::CAP;
+    A.im = A.re + C::AH;
+    coef = reinterpret_cast<int32_t *>(A.im + C::AH);
+  } else {
+    A.re = reinterpret_cast<V *>(kp.ascratch) + (size_t)blockIdx.x * 2 * C::AH;
+    A.im = A.re + C::AH;
+    coef = reinterpret_cast<int32_t *>(smem + C::STATE_BYTES);
+  }
+  const CI<T> *tw = reinterpret_cast<const CI<T> *>(kp.tw);
+  const int n = kp.n;
+  constexpr int LlastF = fwdL(PL, PL.nf - 1);
+  constexpr int RlastF = PL.f[PL.nf - 1];
+  constexpr int LlastI = invL(PL, PL.ni - 1);
+  constexpr int QlastI = PL.q[PL.ni - 1];
+
+  for (int pair = blockIdx.x; pair < kp.batch; pair += gridDim.x) {
+    const uint8_t *a = kp.a + (size_t)pair * n;
+    const uint8_t *b = kp.b + (size_t)pair * n;
+    // ---- fwd(a): pass 0 from HBM, in-place passes, last pass into A ----
+    fwd_pass0<T, N, PL.f[0]>(a, n, st);
+    __syncthreads();
+    run_fwd_mids<T, M, 1, 0>(st, A, tw, true);
+    fwd_mid<T, N, RlastF, LlastF>(st, A, tw);
+    __syncthreads();
+    // ---- fwd(b) ----
+    fwd_pass0<T, N, PL.f[0]>(b, n, st);
+    __syncthreads();
+    run_fwd_mids<T, M, 1, 0>(st, A, tw, false);
+    // ---- fwd(b) last + pointwise + inverse pass 0 ----
+    fwd_last_fused<T, N, RlastF, LlastF>(st, A, tw);
+    if (threadIdx.x == 0) {
+      cs.ok = 1;
+      cs.first_bad = 0x7fffffff;
+      cs.maxrad_bits = 0ull;
+    }
+    __syncthreads();
+    run_inv_mids<T, M, 1>(st, tw);
+    // ---- inverse last pass + certify ----
+    double *dump = nullptr;
+    if (kp.dump_slot) {
+      int s = kp.dump_slot[pair];
+      if (s >= 0) dump = kp.intervals + (size_t)s * N * 4;
+    }
+    inv_last<T, N, QlastI, LlastI>(st, tw, n, coef, cs, dump);
+    __syncthreads();
+    const bool certified = cs.ok != 0;
+    carry_store(coef, n, kp.prod + (size_t)pair * 2 * n, certified, cs);
+    if (kp.coeffs) {
+      int64_t *co = kp.coeffs + (size_t)pair * (2 * n - 1);
+      for (int i = threadIdx.x; i < 2 * n - 1; i += blockDim.x) co[i] = coef[i];
+    }
+    if (threadIdx.x == 0) {
+      kp.cert[pair] = certified ? 1 : 0;
+      if (kp.max_radius) kp.max_radius[pair] = __longlong_as_double((long long)cs.maxrad_bits);
+      if (kp.first_bad) kp.first_bad[pair] = certified ? -1 : cs.first_bad;
+    }
+    __syncthreads();
+  }
+}
+
+// n == 1: m = 1, the DFT is the identity; the product a0*b0 is exact
+__global__ void ivm_n1_kernel(KParams kp) {
+  for (int pair = blockIdx.x * blockDim.x + threadIdx.x; pair < kp.batch;
+       pair += gridDim.x * blockDim.x) {
+    int c = (int)kp.a[pair] * (int)kp.b[pair];
+    kp.prod[2 * pair] = (uint8_t)(c & 255);
+    kp.prod[2 * pair + 1] = (uint8_t)(c >> 8);
+    kp.cert[pair] = 1;
+    if (kp.max_radius) kp.max_radius[pair] = 0.0;
+    if (kp.first_bad) kp.first_bad[pair] = -1;
+    if (kp.coeffs) kp.coeffs[pair] = c;
+    if (kp.dump_slot && kp.dump_slot[pair] >= 0) {
+      double *d = kp.intervals + (size_t)kp.dump_slot[pair] * 4;
+      d[0] = c; d[1] = c; d[2] = 0; d[3] = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// seeded digits; must match paper_1006_0405_b200/inputs.py
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return z;
+}
+__device__ __forceinline__ uint64_t rand64(uint64_t seed, uint64_t s, uint64_t i) {
+  return mix64(seed + 0x9E3779B97F4A7C15ull * ((s << 32) + i + 1));
+}
+
+__global__ void ivm_digits_kernel(uint8_t *out, int n, long long batch, uint64_t seed, uint64_t pair0,
+                                  int operand, int kind, const uint8_t *kinds) {
+  const long long total = (long long)n * batch;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long p = e / n;
+    const int i = (int)(e - p * n);
+    const uint64_t s = 2 * (pair0 + (uint64_t)p) + (uint64_t)operand;
+    const int k = kinds ? kinds[p] : kind;
+    const uint64_t r = rand64(seed, s, (uint64_t)i);
+    uint8_t d = (uint8_t)(r >> 56);
+    if (k == 1) d = 255;
+    else if (k == 2) d = ((r & 0xFFFFFFFFull) < 429496730ull) ? d : 0;
+    else if (k == 3 && i == n - 1 && d == 0) d = (uint8_t)(1 + rand64(seed, s, (uint64_t)n) % 255);
+    out[e] = d;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// directed-rounding FMA throughput probe (K8)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void ivm_probe_kernel(T *sink, int iters) {
+  T a0 = T(1) + T(threadIdx.x) * T(1e-7), a1 = a0 + T(1e-3), a2 = a0 + T(2e-3), a3 = a0 + T(3e-3);
+  T a4 = a0 + T(4e-3), a5 = a0 + T(5e-3), a6 = a0 + T(6e-3), a7 = a0 + T(7e-3);
+  const T m = T(0.9999999), c = T(1e-9);
+  for (int it = 0; it < iters; it++) {
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      a0 = DR<T>::fma_ru(a0, m, c); a1 = DR<T>::fma_rd(a1, m, c);
+      a2 = DR<T>::fma_ru(a2, m, c); a3 = DR<T>::fma_rd(a3, m, c);
+      a4 = DR<T>::fma_ru(a4, m, c); a5 = DR<T>::fma_rd(a5, m, c);
+      a6 = DR<T>::fma_ru(a6, m, c); a7 = DR<T>::fma_rd(a7, m, c);
+    }
+  }
+  sink[blockIdx.x * blockDim.x + threadIdx.x] = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+}
+
+}  // namespace ivm
+
+// ---------------------------------------------------------------------------
+// launchers (C++ linkage, used by ivm_api.cu)
+// ---------------------------------------------------------------------------
+namespace ivm {
+
+int upload_w32(const double *w64, const float *w32) {
+  if (cudaMemcpyToSymbol(c_w32_f64, w64, sizeof(CI<double>) * 32) != cudaSuccess) return -1;
+  if (cudaMemcpyToSymbol(c_w32_f32, w32, sizeof(CI<float>) * 32) != cudaSuccess) return -1;
+  return 0;
+}
+
+
+template <typename T, int M>
+static int info_impl(LaunchInfo *li) {
+  using C = Cfg<T, M>;
+  li->threads = C::THREADS;
+  li->smem = C::SMEM;
+  li->a_smem = C::A_SMEM;
+  li->a_bytes_per_cta = C::A_BYTES;
+  auto k = ivm_cta_kernel<T, M>;
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) != cudaSuccess)
+    return -1;
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, C::THREADS, C::SMEM) != cudaSuccess) return -1;
+  li->blocks_per_sm = nb;
+  return 0;
+}
+
+template <typename T, int M>
+static int launch_impl(const KParams &kp, int grid, cudaStream_t s) {
+  using C = Cfg<T, M>;
+  ivm_cta_kernel<T, M><<<grid, C::THREADS, C::SMEM, s>>>(kp);
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
+}
+
+#define IVM_DISPATCH(FN, T, M, ...)                 \
+  switch (M) {                                      \
+    case 2: return FN<T, 2>(__VA_ARGS__);           \
+    case 3: return FN<T, 3>(__VA_ARGS__);           \
+    case 4: return FN<T, 4>(__VA_ARGS__);           \
+    case 5: return FN<T, 5>(__VA_ARGS__);           \
+    case 6: return FN<T, 6>(__VA_ARGS__);           \
+    case 7: return FN<T, 7>(__VA_ARGS__);           \
+    case 8: return FN<T, 8>(__VA_ARGS__);           \
+    case 9: return FN<T, 9>(__VA_ARGS__);           \
+    case 10: return FN<T, 10>(__VA_ARGS__);         \
+    case 11: return FN<T, 11>(__VA_ARGS__);         \
+    case 12: return FN<T, 12>(__VA_ARGS__);         \
+    case 13: return FN<T, 13>(__VA_ARGS__);         \
+    default: return -4;                             \
+  }
+
+int cta_info(int prec, int m, LaunchInfo *li) {
+  if (prec == 0) { IVM_DISPATCH(info_impl, double, m, li) }
+  else { IVM_DISPATCH(info_impl, float, m, li) }
+}
+
+int cta_launch(int prec, int m, const KParams &kp, int grid, cudaStream_t s) {
+  if (prec == 0) { IVM_DISPATCH(launch_impl, double, m, kp, grid, s) }
+  else { IVM_DISPATCH(launch_impl, float, m, kp, grid, s) }
+}
+
+int n1_launch(const KParams &kp, cudaStream_t s) {
+  int grid = (kp.batch + 255) / 256;
+  if (grid > 1024) grid = 1024;
+  ivm_n1_kernel<<<grid, 256, 0, s>>>(kp);
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
+}
+
+int digits_launch(uint8_t *out, int n, long long batch, uint64_t seed, uint64_t pair0, int operand,
+                  int kind, const uint8_t *kinds, int sms, cudaStream_t s) {
+  long long total = (long long)n * batch;
+  long long grid = (total + 255) / 256;
+  if (grid > (long long)sms * 16) grid = (long long)sms * 16;
+  if (grid < 1) grid = 1;
+  ivm_digits_kernel<<<(int)grid, 256, 0, s>>>(out, n, batch, seed, pair0, operand, kind, kinds);
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
+}
+
+__global__ void ivm_dump_map_kernel(int32_t *slot, int batch, const int32_t *pairs, int n_dump) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n_dump; j += gridDim.x * blockDim.x) {
+    int p = pairs[j];
+    if (p >= 0 && p < batch) slot[p] = j;
+  }
+}
+
+int dump_map_launch(int32_t *slot, int batch, const int32_t *pairs, int n_dump, cudaStream_t s) {
+  if (cudaMemsetAsync(slot, 0xff, sizeof(int32_t) * (size_t)batch, s) != cudaSuccess) return -1;
+  ivm_dump_map_kernel<<<(n_dump + 255) / 256, 256, 0, s>>>(slot, batch, pairs, n_dump);
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
+}
+
+int probe_launch(int prec, int iters, void *sink, int sms, cudaStream_t s, uint64_t *count) {
+  const int threads = 1024, blocks = sms;
+  if (prec == 0) ivm_probe_kernel<double><<<blocks, threads, 0, s>>>((double *)sink, iters);
+  else ivm_probe_kernel<float><<<blocks, threads, 0, s>>>((float *)sink, iters);
+  *count = (uint64_t)blocks * threads * (uint64_t)iters * 64ull;
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
+}
+
+}  // namespace ivm
