@@ -22,9 +22,9 @@ NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--ft
                   "-I", os.path.join(ROOT, "include")]
 CXXFLAGS = ["-O2", "-fPIC", "-std=gnu++17", "-fext-numeric-literals", "-I", os.path.join(ROOT, "include")]
 
-CU = ["ivm_kernels.cu", "ivm_api.cu"]
+CU = ["ivm_kernels.cu", "ivm_v3.cu", "ivm_api.cu"]
 CPP = ["ivm_planner.cpp"]
-HDR = ["ivm_interval.cuh", "ivm_fft.cuh", "ivm_internal.h"]
+HDR = ["ivm_interval.cuh", "ivm_fft.cuh", "ivm_internal.h", "ivm_carry.cuh", "ivm_v3.cuh"]
 
 
 def _stale(obj: str, src: str) -> bool:
@@ -38,19 +38,27 @@ def _stale(obj: str, src: str) -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     objs = []
+    jobs = []
     for f in CU:
         src, obj = os.path.join(CSRC, f), os.path.join(OBJ, f + ".o")
         if force or _stale(obj, src):
             cmd = [NVCC, *NVFLAGS, "-c", src, "-o", obj]
-            r = subprocess.run(cmd, capture_output=True, text=True)
-            if r.returncode != 0:
-                sys.stderr.write(r.stdout + r.stderr)
-                raise RuntimeError(f"nvcc failed on {f}")
-            with open(obj + ".ptxas.txt", "w") as fh:
-                fh.write(r.stderr)
-            if verbose:
-                sys.stderr.write(r.stderr)
+            jobs.append((f, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                                  text=True)))
         objs.append(obj)
+    failed = None
+    for f, obj, pr in jobs:
+        out, err = pr.communicate()
+        if pr.returncode != 0:
+            sys.stderr.write(out + err)
+            failed = f
+            continue
+        with open(obj + ".ptxas.txt", "w") as fh:
+            fh.write(err)
+        if verbose:
+            sys.stderr.write(err)
+    if failed:
+        raise RuntimeError(f"nvcc failed on {failed}")
     for f in CPP:
         src, obj = os.path.join(CSRC, f), os.path.join(OBJ, f + ".o")
         if force or _stale(obj, src):

@@ -20,8 +20,11 @@ struct ivm_ctx {
   int sms = 0;
   int sticky = 0;
   bool consts = false;
-  std::map<std::pair<int, int>, void *> tw;  // (log2m, prec) -> device table
+  std::map<std::pair<int, int>, void *> tw;  // (log2m, prec) -> device table (v1)
+  std::map<std::pair<int, int>, void *> tw3;  // (log2m, prec) -> v3 per-pass tables
   std::map<std::pair<int, int>, ivm::LaunchInfo> info;
+  std::map<std::pair<int, int>, ivm::LaunchInfo> info3;
+  bool force_v1 = false;
   void *ascratch = nullptr;
   size_t ascratch_bytes = 0;
   int32_t *slot = nullptr;
@@ -94,6 +97,20 @@ int ivm_create(ivm_ctx_t *ctx, int device) {
     delete c;
     return IVM_ECUDA;
   }
+  {
+    double t64[64 * 4];
+    float t32[64 * 4];
+    if (ivm::plan_twiddles(6, 0, t64) != 0 || ivm::plan_twiddles(6, 1, t32) != 0) {
+      delete c;
+      return IVM_EUNSUPPORTED;
+    }
+    if (ivm::upload_w64(t64, t32) != 0) {
+      delete c;
+      return IVM_ECUDA;
+    }
+  }
+  const char *kv = getenv("IVM_KERNEL");
+  c->force_v1 = kv && strcmp(kv, "v1") == 0;
   c->consts = true;
   *ctx = c;
   return IVM_OK;
@@ -103,6 +120,7 @@ int ivm_destroy(ivm_ctx_t c) {
   if (!c) return IVM_OK;
   cudaSetDevice(c->device);
   for (auto &kv : c->tw) cudaFree(kv.second);
+  for (auto &kv : c->tw3) cudaFree(kv.second);
   cudaFree(c->ascratch);
   cudaFree(c->slot);
   cudaFree(c->stage);
@@ -128,6 +146,47 @@ static int get_table(ivm_ctx_t c, int m, int prec, const void **out) {
   }
   c->tw[key] = d;
   *out = d;
+  return IVM_OK;
+}
+
+static bool use_v3(ivm_ctx_t c, int m) { return !c->force_v1 && m >= 10 && m <= 13; }
+
+static int get_table3(ivm_ctx_t c, int m, int prec, const void **out) {
+  auto key = std::make_pair(m, prec);
+  auto it = c->tw3.find(key);
+  if (it != c->tw3.end()) {
+    *out = it->second;
+    return IVM_OK;
+  }
+  const size_t N2 = (size_t)2 << m, es = prec == IVM_F64 ? 8 : 4;
+  std::vector<unsigned char> w2N(N2 * 4 * es);
+  if (ivm::plan_twiddles(m + 1, prec, w2N.data()) != 0) return IVM_EUNSUPPORTED;
+  const int ent = ivm::v3_table_entries(m);
+  if (ent < 0) return IVM_EUNSUPPORTED;
+  std::vector<unsigned char> h((size_t)ent * 2 * es);  // compact entries
+  if (ivm::v3_tables(m, prec, w2N.data(), h.data()) != ent) return IVM_EUNSUPPORTED;
+  void *d = nullptr;
+  if (cudaMalloc(&d, h.size()) != cudaSuccess) return IVM_ENOMEM;
+  if (cudaMemcpy(d, h.data(), h.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(d);
+    return cuda_fail(c);
+  }
+  c->tw3[key] = d;
+  *out = d;
+  return IVM_OK;
+}
+
+static int get_info3(ivm_ctx_t c, int m, int prec, ivm::LaunchInfo *li) {
+  auto key = std::make_pair(m, prec);
+  auto it = c->info3.find(key);
+  if (it != c->info3.end()) {
+    *li = it->second;
+    return IVM_OK;
+  }
+  int r = ivm::v3_info(prec, m, li);
+  if (r == -4) return IVM_EUNSUPPORTED;
+  if (r != 0 || li->blocks_per_sm < 1) return cuda_fail(c);
+  c->info3[key] = *li;
   return IVM_OK;
 }
 
@@ -178,10 +237,17 @@ int ivm_reserve(ivm_ctx_t c, size_t n, size_t batch, int prec) {
   int m = log2m_for(n);
   if (m < 2) return IVM_OK;
   const void *t;
-  int r = get_table(c, m, prec, &t);
-  if (r) return r;
   ivm::LaunchInfo li;
-  r = get_info(c, m, prec, &li);
+  int r;
+  if (use_v3(c, m)) {
+    r = get_table3(c, m, prec, &t);
+    if (r) return r;
+    r = get_info3(c, m, prec, &li);
+  } else {
+    r = get_table(c, m, prec, &t);
+    if (r) return r;
+    r = get_info(c, m, prec, &li);
+  }
   if (r) return r;
   if (!li.a_smem) return ensure_scratch(c, (size_t)grid_for(c, li, batch) * li.a_bytes_per_cta);
   return IVM_OK;
@@ -221,10 +287,17 @@ int ivm_multiply_batched_diag(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, s
     return IVM_OK;
   }
   const void *tw;
-  r = get_table(c, m, prec, &tw);
-  if (r) return r;
   ivm::LaunchInfo li;
-  r = get_info(c, m, prec, &li);
+  const bool v3 = use_v3(c, m);
+  if (v3) {
+    r = get_table3(c, m, prec, &tw);
+    if (r) return r;
+    r = get_info3(c, m, prec, &li);
+  } else {
+    r = get_table(c, m, prec, &tw);
+    if (r) return r;
+    r = get_info(c, m, prec, &li);
+  }
   if (r) return r;
   int grid = grid_for(c, li, batch);
   if (!li.a_smem) {
@@ -233,7 +306,8 @@ int ivm_multiply_batched_diag(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, s
     kp.ascratch = c->ascratch;
   }
   kp.tw = tw;
-  if (ivm::cta_launch(prec, m, kp, grid, s) != 0) return cuda_fail(c);
+  if ((v3 ? ivm::v3_launch(prec, m, kp, grid, s) : ivm::cta_launch(prec, m, kp, grid, s)) != 0)
+    return cuda_fail(c);
   c->last_launches = launches + 1;
   return IVM_OK;
 }

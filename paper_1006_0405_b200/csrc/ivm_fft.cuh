@@ -22,8 +22,10 @@ template <> __device__ __forceinline__ const CI<double> &cw32<double>(int j) { r
 template <> __device__ __forceinline__ const CI<float> &cw32<float>(int j) { return c_w32_f32[j]; }
 
 __host__ __device__ constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c(x / 2); }
-__host__ __device__ constexpr int brev(int i, int bits) {
-  return bits == 0 ? 0 : (((i & 1) << (bits - 1)) | brev(i >> 1, bits - 1));
+__host__ __device__ constexpr int brev(int i, int bits) {  // non-recursive: folds after unrolling
+  int r = 0;
+  for (int b = 0; b < bits; b++) r |= ((i >> b) & 1) << (bits - 1 - b);
+  return r;
 }
 
 // t = w_M^j * o (INV: conj(w)), M a power of two <= 32, j < M/2

@@ -36,5 +36,11 @@ int digits_launch(uint8_t *out, int n, long long batch, uint64_t seed, uint64_t 
 int probe_launch(int prec, int iters, void *sink, int sms, cudaStream_t s, uint64_t *count);
 int dump_map_launch(int32_t *slot, int batch, const int32_t *pairs, int n_dump, cudaStream_t s);
 int plan_twiddles(int m, int prec, void *out);
+// v3 (odd-frequency, balanced) path
+int upload_w64(const double *w64, const float *w32);
+int v3_table_entries(int m);
+int v3_tables(int m, int prec, const void *w2N, void *out);
+int v3_info(int prec, int m, LaunchInfo *li);
+int v3_launch(int prec, int m, const KParams &kp, int grid, cudaStream_t s);
 
 }  // namespace ivm

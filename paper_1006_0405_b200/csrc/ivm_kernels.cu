@@ -23,6 +23,7 @@
 
 #include "ivm_fft.cuh"
 #include "ivm_internal.h"
+#include "ivm_carry.cuh"
 
 namespace ivm {
 
@@ -362,72 +363,6 @@ __device__ void inv_last(Arr<T> st, const CI<T> *__restrict__ tw, int n, int32_t
 }
 
 // ---------------------------------------------------------------------------
-// carry: c_i < 2^31 split into bytes; t_i = sum_b byte_b(c_{i-b})
-// <= 1020; u_i = (t_i & 255) + (t_{i-1} >> 8) <= 258; then binary carries
-// with generate u >= 256 / propagate u == 255 (carry-lookahead by ballots).
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ int coef_at(const int32_t *coef, int i, int nc) {
-  return (i >= 0 && i < nc) ? coef[i] : 0;
-}
-__device__ __forceinline__ int t_at(const int32_t *coef, int i, int nc) {
-  int t = 0;
-#pragma unroll
-  for (int b = 0; b < 4; b++) t += (coef_at(coef, i - b, nc) >> (8 * b)) & 255;
-  return t;
-}
-__device__ __forceinline__ int u_at(const int32_t *coef, int i, int nc) {
-  return (t_at(coef, i, nc) & 255) + (t_at(coef, i - 1, nc) >> 8);
-}
-
-__device__ void carry_store(const int32_t *coef, int n, uint8_t *__restrict__ out, bool certified,
-                            CertShared &cs) {
-  const int nout = 2 * n;
-  if (!certified) {
-    for (int i = threadIdx.x; i < nout; i += blockDim.x) out[i] = 0;
-    return;
-  }
-  const int nc = 2 * n - 1, npos = 2 * n + 4;
-  const int T = blockDim.x, K = (npos + T - 1) / T;
-  const int p0 = threadIdx.x * K, p1 = min(p0 + K, npos);
-  // chunk generate / propagate
-  int c = 0;
-  bool allp = true;
-  for (int i = p0; i < p1; i++) {
-    int u = u_at(coef, i, nc);
-    allp = allp && (u == 255);
-    c = (u + c) >> 8;
-  }
-  const bool G = c != 0, Pp = allp;
-  const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = (T + 31) >> 5;
-  const unsigned g = __ballot_sync(0xffffffffu, G), p = __ballot_sync(0xffffffffu, Pp);
-  __shared__ unsigned wg[32], wp[32], wc[32];
-  if (lane == 0) {
-    unsigned long long s = (unsigned long long)(g | p) + g;
-    wg[warp] = (unsigned)(s >> 32);
-    wp[warp] = (p == 0xffffffffu);
-  }
-  __syncthreads();
-  if (warp == 0) {
-    bool gg = lane < nwarps ? wg[lane] != 0 : false;
-    bool pp = lane < nwarps ? wp[lane] != 0 : true;
-    unsigned G2 = __ballot_sync(0xffffffffu, gg), P2 = __ballot_sync(0xffffffffu, pp);
-    unsigned cin = ((G2 | P2) + G2) ^ P2;
-    if (lane < nwarps) wc[lane] = (cin >> lane) & 1u;
-  }
-  __syncthreads();
-  const unsigned c0 = wc[warp];
-  const unsigned long long s = (unsigned long long)(g | p) + g + c0;
-  const unsigned cin_vec = (unsigned)s ^ p;
-  int cc = (cin_vec >> lane) & 1u;
-  for (int i = p0; i < p1; i++) {
-    int u = u_at(coef, i, nc) + cc;
-    if (i < nout) out[i] = (uint8_t)(u & 255);
-    cc = u >> 8;
-  }
-  (void)cs;
-}
-
-// ---------------------------------------------------------------------------
 // the fused CTA kernel
 // ---------------------------------------------------------------------------
 
@@ -523,7 +458,7 @@ __global__ void __launch_bounds__(Cfg<T, M>::THREADS, 1) ivm_cta_kernel(KParams 
     inv_last<T, N, QlastI, LlastI>(st, tw, n, coef, cs, dump);
     __syncthreads();
     const bool certified = cs.ok != 0;
-    carry_store(coef, n, kp.prod + (size_t)pair * 2 * n, certified, cs);
+    carry_store(coef, n, kp.prod + (size_t)pair * 2 * n, certified);
     if (kp.coeffs) {
       int64_t *co = kp.coeffs + (size_t)pair * (2 * n - 1);
       for (int i = threadIdx.x; i < 2 * n - 1; i += blockDim.x) co[i] = coef[i];
@@ -610,17 +545,17 @@ __global__ void ivm_probe_kernel(T *sink, int iters) {
 
 }  // namespace ivm
 
+namespace ivm {
+
 // ---------------------------------------------------------------------------
 // launchers (C++ linkage, used by ivm_api.cu)
 // ---------------------------------------------------------------------------
-namespace ivm {
 
 int upload_w32(const double *w64, const float *w32) {
   if (cudaMemcpyToSymbol(c_w32_f64, w64, sizeof(CI<double>) * 32) != cudaSuccess) return -1;
   if (cudaMemcpyToSymbol(c_w32_f32, w32, sizeof(CI<float>) * 32) != cudaSuccess) return -1;
   return 0;
 }
-
 
 template <typename T, int M>
 static int info_impl(LaunchInfo *li) {

@@ -1,0 +1,154 @@
+// ivm_v3.cu -- translation unit of the balanced odd-frequency kernels (ivm_v3.cuh)
+// and their host-side tables / launchers.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include "ivm_interval.cuh"
+#include "ivm_internal.h"
+#include "ivm_carry.cuh"
+#include "ivm_v3.cuh"
+
+namespace ivm {
+
+// compact first-quadrant entry (lower endpoints); the upper endpoints must be
+// the next representable numbers with the same high 32-bit word (double) --
+// otherwise the plan fails (never observed for m <= 15; tested).
+template <typename F> static bool hi_ok(F lo, F hi) {
+  if (lo == hi) return true;  // exact: the kernel uses next(lo) >= hi, sound
+  if (sizeof(F) == 8) {
+    uint64_t l, h;
+    memcpy(&l, &lo, 8);
+    memcpy(&h, &hi, 8);
+    return h == l + 1 && (h >> 32) == (l >> 32);
+  }
+  uint32_t l, h;
+  memcpy(&l, &lo, 4);
+  memcpy(&h, &hi, 4);
+  return h == l + 1;
+}
+
+// w = full-circle enclosure (re.lo, re.hi, im.lo, im.hi) in the upper half
+// plane -> (c.lo, s.lo with the sign bit = k) where w = i^k (c + i s)
+template <typename F> static bool compact(const F *w, F *o) {
+  F cl = w[0], ch = w[1], sl = w[2], sh = w[3];
+  if (!(sl >= 0)) return false;  // not in the upper half plane
+  unsigned k = 0;
+  if (ch < 0 || (ch == 0 && cl < 0)) {  // second quadrant: w = i (s - i c)
+    F ncl = -ch, nch = -cl;
+    cl = sl; ch = sh; sl = ncl; sh = nch;
+    k = 1;
+  }
+  if (cl == 0) cl = 0;
+  if (sl == 0) sl = 0;
+  if (!hi_ok(cl, ch) || !hi_ok(sl, sh)) return false;
+  o[0] = cl;
+  o[1] = k ? -sl : sl;
+  if (k && sl == 0) {  // -0.0 carries the flag
+    F z = 0;
+    o[1] = -z;
+  }
+  return true;
+}
+
+int upload_w64(const double *w64, const float *w32) {  // full-circle w_64^j tables [64][4]
+  v3::TwC<double> d[17];
+  v3::TwC<float> f[17];
+  for (int j = 0; j <= 16; j++) {
+    double o[2];
+    float of[2];
+    if (!compact(w64 + 4 * j, o) || !compact(w32 + 4 * j, of)) return -4;
+    d[j] = v3::TwC<double>{o[0], o[1]};
+    f[j] = v3::TwC<float>{of[0], of[1]};
+  }
+  if (cudaMemcpyToSymbol(v3::c_w64_f64, d, sizeof(d)) != cudaSuccess) return -1;
+  if (cudaMemcpyToSymbol(v3::c_w64_f32, f, sizeof(f)) != cudaSuccess) return -1;
+  return 0;
+}
+
+// ---- v3 twiddle tables (host): compact entries [2] per twiddle ----
+template <typename F, int M>
+static int v3_tables_impl(const F *w2N /* [2N][4] */, F *out) {
+  using Gm = v3::G3<M>;
+  constexpr int N = Gm::N;
+  constexpr v3::Plan P = v3::plan(M);
+  const long N2 = 2L * N;
+  bool ok = true;
+  auto put = [&](int idx, long e) { ok = ok && compact(w2N + 4L * (((e % N2) + N2) % N2), out + 2L * idx); };
+  for (int p = 1; p < P.nf; p++) {  // forward: w_{2LR}^{q(2k0+1)} = w_{2N}^{q(2k0+1)S'}
+    const int R = P.f[p], L = v3::fL(P, p), Sp = N / (L * R);
+    for (int q = 1; q < R; q++)
+      for (int k0 = 0; k0 < L / 2; k0++) put(Gm::tw_fwd(p) + (q - 1) * (L / 2) + k0, (long)q * (2 * k0 + 1) * Sp);
+  }
+  for (int p = 1; p < P.ni; p++) {  // inverse: w_{LQ} = w_{2N}^{2S'} (direct entries conj'd in-kernel)
+    const int Q = P.q[p], L = v3::iL(P, p), Sp = N / (L * Q);
+    for (int q = 1; q < Q; q++)
+      for (int k0 = 0; k0 < L; k0++) {
+        if (2 * q < Q) put(Gm::tw_inv(p) + (q - 1) * L + k0, 2L * q * k0 * Sp);
+        else put(Gm::tw_inv(p) + (q - 1) * L + k0, 2L * (Q - q) * k0 * Sp);
+      }
+  }
+  for (int k = 0; k < N / 2; k++) put(Gm::tw_fin() + k, k);  // z^k (conj'd in-kernel)
+  return ok ? Gm::tw_total() : -4;
+}
+
+#define IVM_V3_DISPATCH(FN, ...)                    \
+  switch (m) {                                      \
+    case 4: return FN<4>(__VA_ARGS__);              \
+    case 5: return FN<5>(__VA_ARGS__);              \
+    case 6: return FN<6>(__VA_ARGS__);              \
+    case 7: return FN<7>(__VA_ARGS__);              \
+    case 8: return FN<8>(__VA_ARGS__);              \
+    case 9: return FN<9>(__VA_ARGS__);              \
+    case 10: return FN<10>(__VA_ARGS__);            \
+    case 11: return FN<11>(__VA_ARGS__);            \
+    case 12: return FN<12>(__VA_ARGS__);            \
+    case 13: return FN<13>(__VA_ARGS__);            \
+    default: return -4;                             \
+  }
+
+template <int M> static int v3_table_size_m() { return v3::G3<M>::tw_total(); }
+int v3_table_entries(int m) { IVM_V3_DISPATCH(v3_table_size_m) }
+
+template <int M> static int v3_tables_m(int prec, const void *w2N, void *out) {
+  return prec == 0 ? v3_tables_impl<double, M>((const double *)w2N, (double *)out)
+                   : v3_tables_impl<float, M>((const float *)w2N, (float *)out);
+}
+int v3_tables(int m, int prec, const void *w2N, void *out) { IVM_V3_DISPATCH(v3_tables_m, prec, w2N, out) }
+
+template <typename T, int M>
+static int v3_info_impl(LaunchInfo *li) {
+  using C = v3::Cfg3<T, M>;
+  li->threads = C::THREADS;
+  li->smem = C::SMEM;
+  li->a_smem = false;
+  li->a_bytes_per_cta = C::A_BYTES;
+  auto k = v3::ivm_v3_kernel<T, M>;
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) != cudaSuccess)
+    return -1;
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, C::THREADS, C::SMEM) != cudaSuccess) return -1;
+  li->blocks_per_sm = nb;
+  return 0;
+}
+template <int M> static int v3_info_m(int prec, LaunchInfo *li) {
+  return prec == 0 ? v3_info_impl<double, M>(li) : v3_info_impl<float, M>(li);
+}
+int v3_info(int prec, int m, LaunchInfo *li) { IVM_V3_DISPATCH(v3_info_m, prec, li) }
+
+template <int M> static int v3_launch_m(int prec, const KParams &kp, int grid, cudaStream_t s) {
+  if (prec == 0) {
+    using C = v3::Cfg3<double, M>;
+    v3::ivm_v3_kernel<double, M><<<grid, C::THREADS, C::SMEM, s>>>(kp);
+  } else {
+    using C = v3::Cfg3<float, M>;
+    v3::ivm_v3_kernel<float, M><<<grid, C::THREADS, C::SMEM, s>>>(kp);
+  }
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
+}
+int v3_launch(int prec, int m, const KParams &kp, int grid, cudaStream_t s) {
+  IVM_V3_DISPATCH(v3_launch_m, prec, kp, grid, s)
+}
+
+
+}  // namespace ivm
