@@ -13,7 +13,7 @@
 
 #include "ivm_internal.h"
 
-static const int kMaxLog2M = 13;  // CTA-resident path
+static const int kMaxLog2M = 18;  // 13: CTA-resident; 14..18: multi-CTA groups
 
 struct ivm_ctx {
   int device = 0;
@@ -32,6 +32,8 @@ struct ivm_ctx {
   uint8_t *stage = nullptr;  // host API staging: a | b | prod | cert
   size_t stage_bytes = 0;
   int last_launches = 0;
+  void *gscratch = nullptr;  // large-m group scratch
+  size_t gscratch_bytes = 0;
 };
 
 static int cuda_fail(ivm_ctx_t c) {
@@ -124,6 +126,7 @@ int ivm_destroy(ivm_ctx_t c) {
   cudaFree(c->ascratch);
   cudaFree(c->slot);
   cudaFree(c->stage);
+  cudaFree(c->gscratch);
   delete c;
   return IVM_OK;
 }
@@ -150,6 +153,7 @@ static int get_table(ivm_ctx_t c, int m, int prec, const void **out) {
 }
 
 static bool use_v3(ivm_ctx_t c, int m) { return !c->force_v1 && m >= 10 && m <= 13; }
+static bool use_v3g(int m) { return m >= 14 && m <= 18; }
 
 static int get_table3(ivm_ctx_t c, int m, int prec, const void **out) {
   auto key = std::make_pair(m, prec);
@@ -236,6 +240,10 @@ int ivm_reserve(ivm_ctx_t c, size_t n, size_t batch, int prec) {
   if (cudaSetDevice(c->device) != cudaSuccess) return cuda_fail(c);
   int m = log2m_for(n);
   if (m < 2) return IVM_OK;
+  if (use_v3g(m)) {
+    const void *t3;
+    return get_table3(c, m, prec, &t3);
+  }
   const void *t;
   ivm::LaunchInfo li;
   int r;
@@ -283,6 +291,41 @@ int ivm_multiply_batched_diag(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, s
   int m = log2m_for(n);
   if (m == 0) {
     if (ivm::n1_launch(kp, s) != 0) return cuda_fail(c);
+    c->last_launches = launches + 1;
+    return IVM_OK;
+  }
+  if (use_v3g(m)) {
+    const void *tw;
+    r = get_table3(c, m, prec, &tw);
+    if (r) return r;
+    ivm::GroupInfo gi;
+    if (ivm::v3g_info(prec, m, &gi) != 0 || gi.blocks_per_sm < 1) return cuda_fail(c);
+    size_t groups = (size_t)c->sms * gi.blocks_per_sm / gi.C;
+    if (groups > batch) groups = batch;
+    if (groups < 1) return IVM_EUNSUPPORTED;
+    const size_t al = 256;
+    auto up = [&](size_t x) { return (x + al - 1) / al * al; };
+    const size_t b_state = up(groups * gi.state_bytes_per_group), b_coef = up(groups * gi.coef_bytes_per_group);
+    const size_t b_cert = up(groups * 16), b_agg = up(groups * gi.C * 4), b_ctr = up(groups * 4);
+    const size_t need = b_state + b_coef + b_cert + b_agg + b_ctr;
+    if (c->gscratch_bytes < need) {
+      cudaFree(c->gscratch);
+      c->gscratch = nullptr;
+      c->gscratch_bytes = 0;
+      if (cudaMalloc(&c->gscratch, need) != cudaSuccess) return IVM_ENOMEM;
+      c->gscratch_bytes = need;
+    }
+    char *g = (char *)c->gscratch;
+    ivm::GroupArgs ga;
+    ga.state = g;
+    ga.coef = (long long *)(g + b_state);
+    ga.cert = (int *)(g + b_state + b_coef);
+    ga.agg = (unsigned *)(g + b_state + b_coef + b_cert);
+    ga.ctr = (unsigned *)(g + b_state + b_coef + b_cert + b_agg);
+    ga.C = gi.C;
+    if (cudaMemsetAsync(ga.ctr, 0, b_ctr, s) != cudaSuccess) return cuda_fail(c);
+    kp.tw = tw;
+    if (ivm::v3g_launch(prec, m, kp, ga, (int)(groups * gi.C), s) != 0) return cuda_fail(c);
     c->last_launches = launches + 1;
     return IVM_OK;
   }

@@ -42,5 +42,22 @@ int v3_table_entries(int m);
 int v3_tables(int m, int prec, const void *w2N, void *out);
 int v3_info(int prec, int m, LaunchInfo *li);
 int v3_launch(int prec, int m, const KParams &kp, int grid, cudaStream_t s);
+// large m (2^14 .. 2^18): one group of C co-resident CTAs per multiplication
+struct GroupInfo {
+  int blocks_per_sm;
+  int C;
+  size_t state_bytes_per_group;
+  size_t coef_bytes_per_group;
+};
+struct GroupArgs {
+  unsigned *ctr;
+  int C;
+  void *state;
+  long long *coef;
+  int *cert;
+  unsigned *agg;
+};
+int v3g_info(int prec, int m, GroupInfo *gi);
+int v3g_launch(int prec, int m, const KParams &kp, const GroupArgs &ga, int grid, cudaStream_t s);
 
 }  // namespace ivm

@@ -8,6 +8,7 @@
 #include "ivm_internal.h"
 #include "ivm_carry.cuh"
 #include "ivm_v3.cuh"
+#include "ivm_v3g.cuh"
 
 namespace ivm {
 
@@ -104,6 +105,11 @@ static int v3_tables_impl(const F *w2N /* [2N][4] */, F *out) {
     case 11: return FN<11>(__VA_ARGS__);            \
     case 12: return FN<12>(__VA_ARGS__);            \
     case 13: return FN<13>(__VA_ARGS__);            \
+    case 14: return FN<14>(__VA_ARGS__);            \
+    case 15: return FN<15>(__VA_ARGS__);            \
+    case 16: return FN<16>(__VA_ARGS__);            \
+    case 17: return FN<17>(__VA_ARGS__);            \
+    case 18: return FN<18>(__VA_ARGS__);            \
     default: return -4;                             \
   }
 
@@ -132,12 +138,18 @@ static int v3_info_impl(LaunchInfo *li) {
   return 0;
 }
 template <int M> static int v3_info_m(int prec, LaunchInfo *li) {
-  return prec == 0 ? v3_info_impl<double, M>(li) : v3_info_impl<float, M>(li);
+  if constexpr (M > 13) {
+    return -4;
+  } else {
+    return prec == 0 ? v3_info_impl<double, M>(li) : v3_info_impl<float, M>(li);
+  }
 }
 int v3_info(int prec, int m, LaunchInfo *li) { IVM_V3_DISPATCH(v3_info_m, prec, li) }
 
 template <int M> static int v3_launch_m(int prec, const KParams &kp, int grid, cudaStream_t s) {
-  if (prec == 0) {
+  if constexpr (M > 13) {
+    return -4;
+  } else if (prec == 0) {
     using C = v3::Cfg3<double, M>;
     v3::ivm_v3_kernel<double, M><<<grid, C::THREADS, C::SMEM, s>>>(kp);
   } else {
@@ -150,5 +162,45 @@ int v3_launch(int prec, int m, const KParams &kp, int grid, cudaStream_t s) {
   IVM_V3_DISPATCH(v3_launch_m, prec, kp, grid, s)
 }
 
+
+
+// ---- large m: group kernel (cooperative) ----
+template <typename T, int M> static int v3g_info_impl(GroupInfo *gi) {
+  auto k = v3::ivm_v3g_kernel<T, M>;
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, 256, 0) != cudaSuccess) return -1;
+  gi->blocks_per_sm = nb;
+  gi->C = (1 << M) / 8192 < 1 ? 1 : (1 << M) / 8192;
+  gi->state_bytes_per_group = (size_t)6 * ((1 << M) / 2) * 2 * sizeof(T);
+  gi->coef_bytes_per_group = (size_t)(1 << M) * 8;
+  return 0;
+}
+template <int M> static int v3g_info_m(int prec, GroupInfo *gi) {
+  if constexpr (M < 14) {
+    return -4;
+  } else {
+    return prec == 0 ? v3g_info_impl<double, M>(gi) : v3g_info_impl<float, M>(gi);
+  }
+}
+int v3g_info(int prec, int m, GroupInfo *gi) { IVM_V3_DISPATCH(v3g_info_m, prec, gi) }
+
+template <int M> static int v3g_launch_m(int prec, const KParams &kp, const GroupArgs &ga, int grid, cudaStream_t s) {
+  if constexpr (M < 14) {
+    return -4;
+  } else {
+    v3::GroupCtx gc{ga.ctr, ga.C, ga.state, ga.coef, ga.cert, ga.agg};
+    KParams k2 = kp;
+    void *args[] = {(void *)&k2, (void *)&gc};
+    cudaError_t e;
+    if (prec == 0)
+      e = cudaLaunchCooperativeKernel((const void *)v3::ivm_v3g_kernel<double, M>, dim3(grid), dim3(256), args, 0, s);
+    else
+      e = cudaLaunchCooperativeKernel((const void *)v3::ivm_v3g_kernel<float, M>, dim3(grid), dim3(256), args, 0, s);
+    return e == cudaSuccess ? 0 : -1;
+  }
+}
+int v3g_launch(int prec, int m, const KParams &kp, const GroupArgs &ga, int grid, cudaStream_t s) {
+  IVM_V3_DISPATCH(v3g_launch_m, prec, kp, ga, grid, s)
+}
 
 }  // namespace ivm

@@ -24,23 +24,29 @@ namespace v3 {
 // (fused with fwd(b)'s last pass); product(f) = m, product(q) * 2 = m.
 // ---------------------------------------------------------------------------
 struct Plan {
-  int nf, f[5];
-  int ni, q[5];
+  int nf, f[6];
+  int ni, q[6];
 };
 
 __host__ __device__ constexpr Plan plan(int m) {
   switch (m) {
-    case 4: return Plan{2, {2, 8, 0, 0, 0}, 1, {8, 0, 0, 0, 0}};
-    case 5: return Plan{2, {2, 16, 0, 0, 0}, 1, {16, 0, 0, 0, 0}};
-    case 6: return Plan{3, {2, 2, 16, 0, 0}, 2, {16, 2, 0, 0, 0}};
-    case 7: return Plan{3, {2, 4, 16, 0, 0}, 2, {16, 4, 0, 0, 0}};
-    case 8: return Plan{3, {2, 8, 16, 0, 0}, 2, {16, 8, 0, 0, 0}};
-    case 9: return Plan{3, {2, 16, 16, 0, 0}, 2, {16, 16, 0, 0, 0}};
-    case 10: return Plan{4, {2, 2, 16, 16, 0}, 3, {16, 16, 2, 0, 0}};
-    case 11: return Plan{4, {2, 4, 16, 16, 0}, 3, {16, 16, 4, 0, 0}};
-    case 12: return Plan{4, {2, 8, 16, 16, 0}, 3, {16, 16, 8, 0, 0}};
-    case 13: return Plan{4, {2, 16, 16, 16, 0}, 3, {16, 16, 16, 0, 0}};
-    default: return Plan{0, {0, 0, 0, 0, 0}, 0, {0, 0, 0, 0, 0}};
+    case 4: return Plan{2, {2, 8, 0, 0, 0, 0}, 1, {8, 0, 0, 0, 0, 0}};
+    case 5: return Plan{2, {2, 16, 0, 0, 0, 0}, 1, {16, 0, 0, 0, 0, 0}};
+    case 6: return Plan{3, {2, 2, 16, 0, 0, 0}, 2, {16, 2, 0, 0, 0, 0}};
+    case 7: return Plan{3, {2, 4, 16, 0, 0, 0}, 2, {16, 4, 0, 0, 0, 0}};
+    case 8: return Plan{3, {2, 8, 16, 0, 0, 0}, 2, {16, 8, 0, 0, 0, 0}};
+    case 9: return Plan{3, {2, 16, 16, 0, 0, 0}, 2, {16, 16, 0, 0, 0, 0}};
+    case 10: return Plan{4, {2, 2, 16, 16, 0, 0}, 3, {16, 16, 2, 0, 0, 0}};
+    case 11: return Plan{4, {2, 4, 16, 16, 0, 0}, 3, {16, 16, 4, 0, 0, 0}};
+    case 12: return Plan{4, {2, 8, 16, 16, 0, 0}, 3, {16, 16, 8, 0, 0, 0}};
+    case 13: return Plan{4, {2, 16, 16, 16, 0, 0}, 3, {16, 16, 16, 0, 0, 0}};
+    // global-memory (multi-CTA) path
+    case 14: return Plan{5, {2, 2, 16, 16, 16, 0}, 4, {16, 16, 16, 2, 0, 0}};
+    case 15: return Plan{5, {2, 4, 16, 16, 16, 0}, 4, {16, 16, 16, 4, 0, 0}};
+    case 16: return Plan{5, {2, 8, 16, 16, 16, 0}, 4, {16, 16, 16, 8, 0, 0}};
+    case 17: return Plan{5, {2, 16, 16, 16, 16, 0}, 4, {16, 16, 16, 16, 0, 0}};
+    case 18: return Plan{6, {2, 2, 16, 16, 16, 16}, 5, {16, 16, 16, 16, 2, 0}};
+    default: return Plan{0, {0, 0, 0, 0, 0, 0}, 0, {0, 0, 0, 0, 0, 0}};
   }
 }
 
