@@ -116,14 +116,14 @@ __device__ __forceinline__ CI<T> twmul(const CI<T> &w, const CI<T> &d) {
 template <typename T> struct RPairs { Pair<T> lo, hi; bool ss; };
 template <typename T>
 __device__ __forceinline__ RPairs<T> rpairs(T xl, T xh, T yl, T yh) {
-  const bool xP = !DR<T>::neg(xl), xN = DR<T>::neg(xh);
-  const bool yP = !DR<T>::neg(yl), yN = DR<T>::neg(yh);
+  // sign bits (-0 counts as negative: harmless, its products are 0)
+  const bool xln = DR<T>::neg(xl), xhn = DR<T>::neg(xh), yln = DR<T>::neg(yl), yhn = DR<T>::neg(yh);
   RPairs<T> r;
-  r.lo.x = yP ? xl : (yN ? xh : (xP ? xh : xl));
-  r.lo.y = xP ? yl : (xN ? yh : (yP ? yh : yl));
-  r.hi.x = yP ? xh : (yN ? xl : (xP ? xh : xl));
-  r.hi.y = xP ? yh : (xN ? yl : (yP ? yh : yl));
-  r.ss = !(xP || xN) && !(yP || yN);
+  r.lo.x = (!yln || (!yhn && xhn)) ? xl : xh;
+  r.lo.y = (!xln || (!xhn && yln)) ? yl : yh;
+  r.hi.x = (!yln || (!yhn && !xln)) ? xh : xl;
+  r.hi.y = (!xln || (!xhn && !yln)) ? yh : yl;
+  r.ss = xln && !xhn && yln && !yhn;  // both straddle zero
   return r;
 }
 template <typename T>

@@ -138,7 +138,7 @@ static int v3_info_impl(LaunchInfo *li) {
   return 0;
 }
 template <int M> static int v3_info_m(int prec, LaunchInfo *li) {
-  if constexpr (M > 13) {
+  if constexpr (M > 13 || M < 10) {
     return -4;
   } else {
     return prec == 0 ? v3_info_impl<double, M>(li) : v3_info_impl<float, M>(li);
@@ -147,7 +147,7 @@ template <int M> static int v3_info_m(int prec, LaunchInfo *li) {
 int v3_info(int prec, int m, LaunchInfo *li) { IVM_V3_DISPATCH(v3_info_m, prec, li) }
 
 template <int M> static int v3_launch_m(int prec, const KParams &kp, int grid, cudaStream_t s) {
-  if constexpr (M > 13) {
+  if constexpr (M > 13 || M < 10) {
     return -4;
   } else if (prec == 0) {
     using C = v3::Cfg3<double, M>;

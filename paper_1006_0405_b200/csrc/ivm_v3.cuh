@@ -407,23 +407,44 @@ struct Cert3 {
   unsigned long long maxrad;
 };
 
+struct CertAcc {  // per-thread; reduced once per multiplication
+  int ok = 1;
+  int bad = 0x7fffffff;
+  double rad = 0.0;
+};
+
 template <typename T>
-__device__ __forceinline__ void certify_real(T lo, T hi, int i, int n, int32_t *coef, Cert3 &cs,
+__device__ __forceinline__ void certify_real(T lo, T hi, int i, int n, int32_t *coef, CertAcc &acc,
                                              double *dump) {
   if (dump) reinterpret_cast<double4 *>(dump)[i] = make_double4((double)lo, (double)hi, 0.0, 0.0);
   if (i >= 2 * n - 1) return;
   const double l = (double)lo, h = (double)hi;
   const double cl = ceil(l);
   const bool ok = cl == floor(h);
-  double rad = __dmul_ru(__dadd_ru(h, -l), 0.5);
-  if (!(rad <= 1e300)) rad = __longlong_as_double(0x7ff0000000000000ll);
-  atomicMax(&cs.maxrad, (unsigned long long)__double_as_longlong(rad));
-  if (ok) {
-    coef[i] = (int32_t)cl;
-  } else {
-    coef[i] = 0;
-    cs.ok = 0;
-    atomicMin(&cs.first_bad, i);
+  const double rad = __dmul_ru(__dadd_ru(h, -l), 0.5);
+  acc.rad = (rad <= acc.rad) ? acc.rad : rad;  // NaN propagates (comparison false)
+  coef[i] = ok ? (int32_t)cl : 0;
+  if (!ok) {
+    acc.ok = 0;
+    acc.bad = min(acc.bad, i);
+  }
+}
+
+__device__ __forceinline__ void cert_flush(const CertAcc &acc, Cert3 &cs) {
+  const int ok = __reduce_and_sync(0xffffffffu, (unsigned)acc.ok);
+  const int bad = (int)__reduce_min_sync(0xffffffffu, (unsigned)acc.bad);
+  double rad = acc.rad;
+  for (int o = 16; o; o >>= 1) {
+    const double r2 = __shfl_xor_sync(0xffffffffu, rad, o);
+    rad = (r2 <= rad) ? rad : r2;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (!ok) {
+      cs.ok = 0;
+      atomicMin(&cs.first_bad, bad);
+    }
+    unsigned long long rb = (rad == rad) ? (unsigned long long)__double_as_longlong(rad) : 0x7ff0000000000000ull;
+    atomicMax(&cs.maxrad, rb);
   }
 }
 
@@ -431,17 +452,17 @@ __device__ __forceinline__ void certify_real(T lo, T hi, int i, int n, int32_t *
 // c_{k+m/2} = 2 Im v / m  (the folded radix-2 step)
 template <typename T, int M>
 __device__ __forceinline__ void emit_coeffs(const CI<T> &o, int k, const TwC<T> *__restrict__ tw, int twi,
-                                            int n, int32_t *coef, Cert3 &cs, double *dump) {
+                                            int n, int32_t *coef, CertAcc &acc, double *dump) {
   constexpr int N = 1 << M;
   const CI<T> v = rtmul<T, true>(ldg_twc(tw, twi), o);  // z^{-k} = conj(z^k)
   const T s = T(2) / T(N);  // exact power of two
-  certify_real(DR<T>::mul_rd(v.rl, s), DR<T>::mul_ru(v.rh, s), k, n, coef, cs, dump);
-  certify_real(DR<T>::mul_rd(v.il, s), DR<T>::mul_ru(v.ih, s), k + N / 2, n, coef, cs, dump);
+  certify_real(DR<T>::mul_rd(v.rl, s), DR<T>::mul_ru(v.rh, s), k, n, coef, acc, dump);
+  certify_real(DR<T>::mul_rd(v.il, s), DR<T>::mul_ru(v.ih, s), k + N / 2, n, coef, acc, dump);
 }
 
 template <typename T, int M>
 __device__ __forceinline__ void inv_last(Buf<T> st, const TwC<T> *__restrict__ tw, int n, int32_t *coef,
-                                         Cert3 &cs, double *dump) {
+                                         CertAcc &acc, double *dump) {
   using Gm = G3<M>;
   constexpr int p = Gm::P.ni - 1, Q = Gm::P.q[p], L = iL(Gm::P, p), G = 16 / Q;
   constexpr int TWF = Gm::tw_fin();
@@ -454,48 +475,7 @@ __device__ __forceinline__ void inv_last(Buf<T> st, const TwC<T> *__restrict__ t
 #pragma unroll
     for (int r = 0; r < Q; r++) {
       const int k = k0s[g] + L * r;
-      emit_coeffs<T, M>(v[g][r], k, tw, TWF + k, n, coef, cs, dump);
-    }
-  }
-}
-
-// fwd(b) last pass + pointwise + inverse pass 0, in registers
-template <typename T, int M>
-__device__ __forceinline__ void fused(Buf<T> st, Buf<T> A, const TwC<T> *__restrict__ tw, int n,
-                                      int32_t *coef, Cert3 &cs, double *dump) {
-  using Gm = G3<M>;
-  constexpr int p = Gm::P.nf - 1, R = Gm::P.f[p], L = fL(Gm::P, p), G = 16 / R;
-  static_assert(Gm::P.q[0] == R, "fused radix");
-  constexpr int TWF = Gm::tw_fin();
-  CI<T> v[G][R];
-  int k0s[G], nus[G];
-  fwd_load_compute<T, M, p>(st, tw, v, k0s, nus);
-#pragma unroll
-  for (int g = 0; g < G; g++) {
-    if (k0s[g] < 0) continue;
-#pragma unroll
-    for (int r = 0; r < R; r++) v[g][r] = cmul(A.ld(r * (L / 2) + k0s[g]), v[g][r]);
-    cdft<T, R, true>(v[g]);
-  }
-  if constexpr (Gm::P.ni == 1) {
-    // the fused pass is also the last inverse pass (S_1 = 2): emit coefficients
-#pragma unroll
-    for (int g = 0; g < G; g++) {
-      if (k0s[g] != 0) continue;
-#pragma unroll
-      for (int r = 0; r < R; r++) {  // S_1 = 2: the single task k0 = 0 holds E_1[r][0]
-        const int k = r;
-        emit_coeffs<T, M>(v[g][r], k, tw, TWF + k, n, coef, cs, dump);
-      }
-    }
-  } else {
-    constexpr int RSo = Gm::iRS(1);
-    __syncthreads();
-#pragma unroll
-    for (int g = 0; g < G; g++) {
-      if (k0s[g] < 0) continue;
-#pragma unroll
-      for (int r = 0; r < R; r++) st.st(r * RSo + k0s[g], v[g][r]);
+      emit_coeffs<T, M>(v[g][r], k, tw, TWF + k, n, coef, acc, dump);
     }
   }
 }
@@ -516,6 +496,99 @@ __device__ __forceinline__ void run_inv(Buf<T> st, const TwC<T> *tw) {
     __syncthreads();
     run_inv<T, M, p + 1>(st, tw);
   }
+}
+
+// ---------------------------------------------------------------------------
+// runtime-parameterised radix-16 pass bodies: ONE code copy serves every
+// forward pass p >= 2 (and the last / fused one) and every inverse pass, so the
+// straight-line kernel stays small enough for the instruction cache.
+// ---------------------------------------------------------------------------
+struct PassRT {
+  int lgSp, L, RSi, RSo, tw;
+};
+
+__host__ __device__ constexpr int ilog2r(int x) { return x <= 1 ? 0 : 1 + ilog2r(x / 2); }
+
+template <int M> struct RT3 {
+  static constexpr int nf = plan(M).nf, ni = plan(M).ni;
+  static constexpr int NFWD = nf - 2;  // forward passes 2 .. nf-1 (all radix 16)
+  static constexpr bool LAST16 = plan(M).q[ni - 1] == 16;
+  static constexpr int NINV = LAST16 ? ni - 1 : ni - 2;  // inverse passes 1 .. via the shared body
+  __host__ __device__ static constexpr PassRT fwd(int i) {
+    return PassRT{ilog2r((1 << M) / fL(plan(M), i + 2) / 16), fL(plan(M), i + 2), G3<M>::fRS(i + 2),
+                  (i + 3 < nf) ? G3<M>::fRS(i + 3) : G3<M>::iRS(1), G3<M>::tw_fwd(i + 2)};
+  }
+  __host__ __device__ static constexpr PassRT inv(int i) {
+    return PassRT{ilog2r((1 << M) / iL(plan(M), i + 1) / 16), iL(plan(M), i + 1), G3<M>::iRS(i + 1),
+                  (i + 2 < ni) ? G3<M>::iRS(i + 2) : 0, G3<M>::tw_inv(i + 1)};
+  }
+};
+
+template <int M>
+__device__ __forceinline__ PassRT pick_fwd(int i) {
+  static_assert(RT3<M>::NFWD >= 1 && RT3<M>::NFWD <= 3, "forward passes");
+  constexpr PassRT p0 = RT3<M>::fwd(0);
+  constexpr PassRT p1 = RT3<M>::fwd(RT3<M>::NFWD > 1 ? 1 : 0);
+  constexpr PassRT p2 = RT3<M>::fwd(RT3<M>::NFWD > 2 ? 2 : 0);
+  return i == 0 ? p0 : (i == 1 ? p1 : p2);
+}
+template <int M>
+__device__ __forceinline__ PassRT pick_inv(int i) {
+  static_assert(RT3<M>::NINV >= 1 && RT3<M>::NINV <= 3, "inverse passes");
+  constexpr PassRT p0 = RT3<M>::inv(0);
+  constexpr PassRT p1 = RT3<M>::inv(RT3<M>::NINV > 1 ? 1 : 0);
+  constexpr PassRT p2 = RT3<M>::inv(RT3<M>::NINV > 2 ? 2 : 0);
+  return i == 0 ? p0 : (i == 1 ? p1 : p2);
+}
+
+// L1 prefetch of the twiddles a thread will read in a later pass
+template <typename T>
+__device__ __forceinline__ void prefetch_tw(const TwC<T> *tw, const PassRT &pp, bool inverse) {
+  const int t = threadIdx.x;
+  const int k0 = inverse ? (t >> (pp.lgSp - 1)) : (t >> pp.lgSp);
+  const int stride = inverse ? pp.L : (pp.L >> 1);
+  const TwC<T> *b = tw + pp.tw + k0;
+#pragma unroll
+  for (int q = 1; q < 16; q++) asm volatile("prefetch.global.L1 [%0];" ::"l"(b + (q - 1) * stride));
+}
+
+// forward: F_p[k0][nu + Sp q] * w_{32L}^{q(2k0+1)} -> 16-point DFT
+template <typename T>
+__device__ __forceinline__ void fwd16(Buf<T> st, const TwC<T> *__restrict__ tw, const PassRT &pp,
+                                      CI<T> (&v)[16], int &k0, int &nu) {
+  const int t = threadIdx.x, Sp = 1 << pp.lgSp;
+  k0 = t >> pp.lgSp;
+  nu = t & (Sp - 1);
+  const int base = k0 * pp.RSi + nu, tb = pp.tw + k0, tstride = pp.L >> 1;
+#pragma unroll
+  for (int q = 0; q < 16; q++) {
+    CI<T> z = st.ld(base + Sp * q);
+    if (q > 0) z = rtmul<T, false>(ldg_twc(tw, tb + (q - 1) * tstride), z);
+    v[q] = z;
+  }
+  cdft<T, 16, false>(v);
+}
+
+// inverse: E_p[k0][mu] (mirror for q >= 8) * twiddle -> 16-point inverse DFT
+template <typename T>
+__device__ __forceinline__ void inv16(Buf<T> st, const TwC<T> *__restrict__ tw, const PassRT &pp,
+                                      CI<T> (&v)[16], int &k0, int &nu) {
+  const int t = threadIdx.x, Sp = 1 << pp.lgSp, lgH = pp.lgSp - 1, S = 16 * Sp;
+  k0 = t >> lgH;
+  nu = t & ((Sp >> 1) - 1);
+  const int base = k0 * pp.RSi, tb = pp.tw + k0;
+#pragma unroll
+  for (int q = 0; q < 16; q++) {
+    CI<T> z;
+    if (q < 8) z = st.ld(base + nu + Sp * q);
+    else z = cconj(st.ld(base + (S - 1 - nu - Sp * q)));
+    if (q > 0) {
+      const TwC<T> w = ldg_twc(tw, tb + (q - 1) * pp.L);
+      z = (q < 8) ? rtmul<T, true>(w, z) : rtmul<T, false>(w, z);
+    }
+    v[q] = z;
+  }
+  cdft<T, 16, true>(v);
 }
 
 template <typename T, int M> struct Cfg3 {
@@ -543,36 +616,80 @@ __global__ void __launch_bounds__(Cfg3<T, M>::THREADS, 1) ivm_v3_kernel(KParams 
   const TwC<T> *tw = reinterpret_cast<const TwC<T> *>(kp.tw);
   const int n = kp.n;
 
+  constexpr int NFWD = RT3<M>::NFWD, NINV = RT3<M>::NINV;
+  constexpr bool LAST16 = RT3<M>::LAST16;
+  constexpr int RSI1 = Gm::iRS(1), TWF = Gm::tw_fin();
+
   for (int pair = blockIdx.x; pair < kp.batch; pair += gridDim.x) {
-    // ---- fwd(a) ----
-    fwd_first<T, M>(kp.a + (size_t)pair * n, n, st, tw);
-    __syncthreads();
-    run_fwd<T, M, 2>(st, tw);
-    fwd_last_a<T, M>(st, A, tw);
-    __syncthreads();
-    // ---- fwd(b) ----
-    fwd_first<T, M>(kp.b + (size_t)pair * n, n, st, tw);
-    if (threadIdx.x == 0) {
-      cs.ok = 1;
-      cs.first_bad = 0x7fffffff;
-      cs.maxrad = 0ull;
-    }
-    __syncthreads();
-    run_fwd<T, M, 2>(st, tw);
     double *dump = nullptr;
     if (kp.dump_slot) {
       const int s = kp.dump_slot[pair];
       if (s >= 0) dump = kp.intervals + (size_t)s * N * 4;
     }
-    fused<T, M>(st, A, tw, n, coef, cs, dump);
-    __syncthreads();
-    if constexpr (Gm::P.ni > 1) {
-      run_inv<T, M, 1>(st, tw);
-      inv_last<T, M>(st, tw, n, coef, cs, dump);
+#pragma unroll 1
+    for (int op = 0; op < 2; op++) {
+      fwd_first<T, M>((op == 0 ? kp.a : kp.b) + (size_t)pair * n, n, st, tw);
+      if (op == 1 && threadIdx.x == 0) {
+        cs.ok = 1;
+        cs.first_bad = 0x7fffffff;
+        cs.maxrad = 0ull;
+      }
+      __syncthreads();
+#pragma unroll 1
+      for (int i = 0; i < NFWD; i++) {
+        const PassRT pp = pick_fwd<M>(i);
+        CI<T> v[16];
+        int k0, nu;
+        if (i + 1 < NFWD) prefetch_tw<T>(tw, pick_fwd<M>(i + 1), false);
+        else if (op == 1) prefetch_tw<T>(tw, pick_inv<M>(0), true);
+        fwd16<T>(st, tw, pp, v, k0, nu);
+        if (i < NFWD - 1) {  // mid pass: store both halves (mirror conjugated)
+          __syncthreads();
+#pragma unroll
+          for (int r = 0; r < 16; r++) {
+            if (r < 8) st.st((k0 + pp.L * r) * pp.RSo + nu, v[r]);
+            else st.st((16 * pp.L - 1 - k0 - pp.L * r) * pp.RSo + nu, cconj(v[r]));
+          }
+        } else if (op == 0) {  // last pass of a: spectrum class k0 -> A
+#pragma unroll
+          for (int r = 0; r < 16; r++) A.st(r * (pp.L >> 1) + k0, v[r]);
+        } else {  // last pass of b + pointwise + inverse pass 0
+#pragma unroll
+          for (int r = 0; r < 16; r++) v[r] = cmul(A.ld(r * (pp.L >> 1) + k0), v[r]);
+          cdft<T, 16, true>(v);
+          __syncthreads();
+#pragma unroll
+          for (int r = 0; r < 16; r++) st.st(r * RSI1 + k0, v[r]);
+        }
+        __syncthreads();
+      }
+    }
+    CertAcc acc;
+#pragma unroll 1
+    for (int i = 0; i < NINV; i++) {
+      const PassRT pp = pick_inv<M>(i);
+      CI<T> v[16];
+      int k0, nu;
+      if (i + 1 < NINV) prefetch_tw<T>(tw, pick_inv<M>(i + 1), true);
+      inv16<T>(st, tw, pp, v, k0, nu);
+      if (!LAST16 || i < NINV - 1) {
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < 16; r++) st.st((k0 + pp.L * r) * pp.RSo + nu, v[r]);
+      } else {
+#pragma unroll
+        for (int r = 0; r < 16; r++) {
+          const int k = k0 + pp.L * r;
+          emit_coeffs<T, M>(v[r], k, tw, TWF + k, n, coef, acc, dump);
+        }
+      }
       __syncthreads();
     }
+    if constexpr (!LAST16) inv_last<T, M>(st, tw, n, coef, acc, dump);
+    cert_flush(acc, cs);
+    __syncthreads();
     const bool certified = cs.ok != 0;
-    carry_store(coef, n, kp.prod + (size_t)pair * 2 * n, certified);
+    carry_store(coef, n, kp.prod + (size_t)pair * 2 * n, certified, reinterpret_cast<uint16_t *>(smem));
     if (kp.coeffs) {
       int64_t *co = kp.coeffs + (size_t)pair * (2 * n - 1);
       for (int i = threadIdx.x; i < 2 * n - 1; i += blockDim.x) co[i] = certified ? coef[i] : 0;
