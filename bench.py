@@ -33,10 +33,14 @@ METRIC = "certified base-256 digits multiplied/sec (fp64 interval FFT); % of roo
 UNIT = "digits/s"
 
 CONFIGS = {
-    # name: (n, batch, prec, kind, workload text)
+    # name: (n, batch, prec, kind (int, or "C3"/"C5" per-pair classes), workload text)
     "C1": (1000, 1, "f64", 3, "C1: one multiplication of two 1,000-digit base-256 integers, fp64, m=2048"),
     "C2": (4096, 4096, "f64", 0, "C2: 4,096 multiplications of 4,096-digit base-256 integers, uniform digits, fp64 intervals, m=8,192"),
+    "C3": (75000, 64, "f64", "C3", "C3: 64 multiplications of 75,000-digit base-256 integers (the paper's limit), half uniform / half all-255, fp64, m=262,144"),
+    "C5": (16384, 65536, "f64", "C5", "C5: 65,536 multiplications of 16,384-digit integers, 1/3 uniform, 1/3 all-255, 1/3 sparse, fp64, m=32,768; batch sharded across ranks"),
 }
+# per-rank batch: C5's batch is the whole job (strong scaling); the others are per rank (weak)
+STRONG = {"C5"}
 
 
 def W_ops(m: int) -> int:
@@ -54,29 +58,57 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region (NVML,
+    every 10 ms; falls back to nvidia-smi)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
+        self.sm, self.mx, self.reasons = [], [], set()
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        except Exception:
+            self._nvml = None
+
+    def _sample_nvml(self):
+        nv = self._nvml
+        self.sm.append(float(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)))
+        self.mx.append(float(nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)))
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        for k, bit in self.REASONS.items():
+            if r & bit:
+                self.reasons.add(k)
+
+    def _sample_smi(self):
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                              "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                              "clocks_event_reasons.hw_thermal_slowdown,"
+                              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip()
+        if out:
+            f = [x.strip() for x in out.split(",")]
+            self.sm.append(float(f[0]))
+            self.mx.append(float(f[1]))
+            for k, v in zip(["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"], f[2:]):
+                if v.lower() == "active":
+                    self.reasons.add(k)
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                self._sample_nvml() if self._nvml else self._sample_smi()
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            self._stop.wait(0.01 if self._nvml else 0.1)
 
     def start(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -86,18 +118,11 @@ class ClockSampler:
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
-        if not self.rows:
+        if not self.sm:
             return None
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in self.rows:
-            for k, nm in enumerate(names):
-                if len(r) > 4 + k and r[4 + k].lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": max(self.mx),
+                "reasons": sorted(self.reasons), "samples": len(self.sm),
+                "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
 def cpu_baseline(a, b, n, prec, budget_s=12.0):
@@ -133,9 +158,9 @@ def run_reference(args):
     n, batch, prec, kind, text = CONFIGS[args.config]
     import oracle
     cores = oracle.max_threads()
-    k = max(cores, 8)
+    k = max(cores, 8) if n < 20000 else max(2, cores // 4)
     pairs = np.arange(k)
-    kinds = np.full(k, kind)
+    kinds = inputs.class_of_pairs(args.config, batch)[:k] if isinstance(kind, str) else np.full(k, kind)
     a, b = inputs.pair_digits(inputs.config_seed(int(args.config[1:])), pairs, n, kinds)
     for _ in range(args.warmup):
         oracle.ivmul(a[:cores], b[:cores], prec=prec)
@@ -148,7 +173,8 @@ def run_reference(args):
     dt = sum(times) / len(times)
     value = cert * n / dt
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "strong" if args.config in STRONG else "weak",
             "vs_baseline": None, "dtype": prec, "data": "synthetic (seeded SplitMix64 digits)",
             "impl": "reference",
             "config": {"workload": text, "n": n, "batch": batch, "fft_length": 1 << math.ceil(math.log2(2 * n - 1)),
@@ -165,6 +191,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_1006_0405_b200 as ivm
+    from paper_1006_0405_b200 import dist as ivd
     from paper_1006_0405_b200 import inputs
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -181,7 +208,13 @@ def run_ours(args):
     seed = inputs.config_seed(int(args.config[1:]))
     ctx = ivm.Context(local)
     s = torch.cuda.current_stream()
-    pair0 = rank * batch  # weak scaling: each rank its own shard
+    if args.config in STRONG:  # the whole job's batch is sharded across ranks
+        pair0, batch = ivd.shard(batch, rank, world)
+    else:  # weak scaling: each rank its own batch
+        pair0 = rank * batch
+    if isinstance(kind, str):
+        kinds_np = inputs.class_of_pairs(kind, CONFIGS[kind][1])[pair0:pair0 + batch].astype(np.uint8)
+        kind = torch.from_numpy(kinds_np).to(dev)
     a = ctx.generate_digits(n, batch, seed, 0, kind=kind, pair0=pair0)
     b = ctx.generate_digits(n, batch, seed, 1, kind=kind, pair0=pair0)
     out = torch.empty((batch, 2 * n), dtype=torch.uint8, device=dev)
@@ -193,12 +226,11 @@ def run_ours(args):
     torch.cuda.synchronize()
     launches_per_step = ctx.last_launch_count
     sampler = ClockSampler(local)
-    sampler.start()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    certified_steps = []
+    sampler.start()
     for i in range(args.steps):
         flush.zero_()
         evs[i][0].record(s)
@@ -211,13 +243,18 @@ def run_ours(args):
     step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
     tot_ms = sum(step_ms)
     ncert = int(cert.sum().item())
-    t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
-    c = torch.tensor([ncert], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(c, op=dist.ReduceOp.SUM)
-    tot_ms = float(t.item())
-    total_cert = float(c.item())
+    tot_ms = ivd.max_over_ranks(tot_ms, device=dev)
+    total_cert = ivd.sum_over_ranks(ncert, device=dev)
+    gather_ms = None
+    if args.gather and world > 1:
+        torch.cuda.synchronize()
+        dist.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(s)
+        ivd.gather_to_root(out, cert)
+        g1.record(s)
+        torch.cuda.synchronize()
+        gather_ms = ivd.max_over_ranks(g0.elapsed_time(g1), device=dev)
     ms_per_step = tot_ms / args.steps
     value = total_cert * n / (ms_per_step / 1e3)
 
@@ -238,10 +275,7 @@ def run_ours(args):
     e1.record(s)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
-    te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_ms = float(te.item())
+    e2e_ms = ivd.max_over_ranks(e2e_ms, device=dev)
     e2e_cert = int(hcert.sum().item()) * world
     e2e_value = e2e_cert * n / (e2e_ms / 1e3)
 
@@ -250,7 +284,7 @@ def run_ours(args):
         sm_max = peaks.get("sm_max_mhz", 1965.0)
         peak_ops = 148 * 64 * sm_max * 1e6  # directed FP64 instr/s (FMA = 1 op), nominal lanes
         kernel_s = ms_per_step / 1e3
-        achieved = W_ops(m) * batch / kernel_s
+        achieved = W_ops(m) * batch / kernel_s  # rank 0's share; ranks run the same shape
         # measured directed-FMA rate (probe), for context
         probe = None
         try:
@@ -273,12 +307,14 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": prec_s,
+            "scaling": "strong" if args.config in STRONG else "weak", "vs_baseline": None, "dtype": prec_s,
             "data": "synthetic (seeded SplitMix64 digits generated on device)",
             "config": {"workload": text, "n": n, "batch_per_gpu": batch, "fft_length": m,
+                       "seed": seed,
                        "parallelism": f"batch-sharded x{world} (no data-path collective)",
                        "l2": "flushed between timed steps (256 MiB write, outside the events)",
-                       "certified_pairs_per_step": total_cert},
+                       "certified_pairs_per_step": total_cert,
+                       "gather_to_rank0_ms": gather_ms},
             "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12,
                          "unit": "Top/s (directed FP64 DADD/DMUL/DFMA, FMA = 1 op)",
                          "frac": achieved / peak_ops, "traffic": None,
@@ -299,11 +335,12 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gather", action="store_true", help="also time the NCCL gather of products to rank 0")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

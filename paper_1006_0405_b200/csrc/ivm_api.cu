@@ -25,6 +25,7 @@ struct ivm_ctx {
   std::map<std::pair<int, int>, ivm::LaunchInfo> info;
   std::map<std::pair<int, int>, ivm::LaunchInfo> info3;
   bool force_v1 = false;
+  int radix = 8;  // radix of the one-CTA kernel (IVM_RADIX=16 for the register-heavy variant)
   void *ascratch = nullptr;
   size_t ascratch_bytes = 0;
   int32_t *slot = nullptr;
@@ -113,6 +114,8 @@ int ivm_create(ivm_ctx_t *ctx, int device) {
   }
   const char *kv = getenv("IVM_KERNEL");
   c->force_v1 = kv && strcmp(kv, "v1") == 0;
+  const char *rv = getenv("IVM_RADIX");
+  if (rv && strcmp(rv, "16") == 0) c->radix = 16;
   c->consts = true;
   *ctx = c;
   return IVM_OK;
@@ -156,7 +159,8 @@ static bool use_v3(ivm_ctx_t c, int m) { return !c->force_v1 && m >= 10 && m <= 
 static bool use_v3g(int m) { return m >= 14 && m <= 18; }
 
 static int get_table3(ivm_ctx_t c, int m, int prec, const void **out) {
-  auto key = std::make_pair(m, prec);
+  const int radix = (m >= 10 && m <= 13) ? c->radix : 16;
+  auto key = std::make_pair(m * 100 + radix, prec);
   auto it = c->tw3.find(key);
   if (it != c->tw3.end()) {
     *out = it->second;
@@ -165,10 +169,10 @@ static int get_table3(ivm_ctx_t c, int m, int prec, const void **out) {
   const size_t N2 = (size_t)2 << m, es = prec == IVM_F64 ? 8 : 4;
   std::vector<unsigned char> w2N(N2 * 4 * es);
   if (ivm::plan_twiddles(m + 1, prec, w2N.data()) != 0) return IVM_EUNSUPPORTED;
-  const int ent = ivm::v3_table_entries(m);
+  const int ent = ivm::v3_table_entries(m, radix);
   if (ent < 0) return IVM_EUNSUPPORTED;
   std::vector<unsigned char> h((size_t)ent * 2 * es);  // compact entries
-  if (ivm::v3_tables(m, prec, w2N.data(), h.data()) != ent) return IVM_EUNSUPPORTED;
+  if (ivm::v3_tables(m, prec, radix, w2N.data(), h.data()) != ent) return IVM_EUNSUPPORTED;
   void *d = nullptr;
   if (cudaMalloc(&d, h.size()) != cudaSuccess) return IVM_ENOMEM;
   if (cudaMemcpy(d, h.data(), h.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
@@ -181,13 +185,13 @@ static int get_table3(ivm_ctx_t c, int m, int prec, const void **out) {
 }
 
 static int get_info3(ivm_ctx_t c, int m, int prec, ivm::LaunchInfo *li) {
-  auto key = std::make_pair(m, prec);
+  auto key = std::make_pair(m * 100 + c->radix, prec);
   auto it = c->info3.find(key);
   if (it != c->info3.end()) {
     *li = it->second;
     return IVM_OK;
   }
-  int r = ivm::v3_info(prec, m, li);
+  int r = ivm::v3_info(prec, m, c->radix, li);
   if (r == -4) return IVM_EUNSUPPORTED;
   if (r != 0 || li->blocks_per_sm < 1) return cuda_fail(c);
   c->info3[key] = *li;
@@ -349,7 +353,7 @@ int ivm_multiply_batched_diag(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, s
     kp.ascratch = c->ascratch;
   }
   kp.tw = tw;
-  if ((v3 ? ivm::v3_launch(prec, m, kp, grid, s) : ivm::cta_launch(prec, m, kp, grid, s)) != 0)
+  if ((v3 ? ivm::v3_launch(prec, m, c->radix, kp, grid, s) : ivm::cta_launch(prec, m, kp, grid, s)) != 0)
     return cuda_fail(c);
   c->last_launches = launches + 1;
   return IVM_OK;

@@ -11,7 +11,7 @@
 namespace ivm {
 
 // coef: [2n-1] int32 (shared); ubuf: >= 2n+4 uint16 scratch (shared)
-static __device__ void carry_store(const int32_t *coef, int n, uint8_t *__restrict__ out, bool certified,
+static __device__ __forceinline__ void carry_store(const int32_t *coef, int n, uint8_t *__restrict__ out, bool certified,
                                    uint16_t *ubuf) {
   const int nout = 2 * n;
   if (!certified) {

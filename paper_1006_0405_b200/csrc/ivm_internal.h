@@ -38,10 +38,10 @@ int dump_map_launch(int32_t *slot, int batch, const int32_t *pairs, int n_dump, 
 int plan_twiddles(int m, int prec, void *out);
 // v3 (odd-frequency, balanced) path
 int upload_w64(const double *w64, const float *w32);
-int v3_table_entries(int m);
-int v3_tables(int m, int prec, const void *w2N, void *out);
-int v3_info(int prec, int m, LaunchInfo *li);
-int v3_launch(int prec, int m, const KParams &kp, int grid, cudaStream_t s);
+int v3_table_entries(int m, int radix);
+int v3_tables(int m, int prec, int radix, const void *w2N, void *out);
+int v3_info(int prec, int m, int radix, LaunchInfo *li);
+int v3_launch(int prec, int m, int radix, const KParams &kp, int grid, cudaStream_t s);
 // large m (2^14 .. 2^18): one group of C co-resident CTAs per multiplication
 struct GroupInfo {
   int blocks_per_sm;

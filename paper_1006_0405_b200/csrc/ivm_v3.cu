@@ -68,11 +68,11 @@ int upload_w64(const double *w64, const float *w32) {  // full-circle w_64^j tab
 }
 
 // ---- v3 twiddle tables (host): compact entries [2] per twiddle ----
-template <typename F, int M>
+template <typename F, int M, int RK>
 static int v3_tables_impl(const F *w2N /* [2N][4] */, F *out) {
-  using Gm = v3::G3<M>;
+  using Gm = v3::G3<M, RK>;
   constexpr int N = Gm::N;
-  constexpr v3::Plan P = v3::plan(M);
+  constexpr v3::Plan P = v3::plan_cta(M, RK);
   const long N2 = 2L * N;
   bool ok = true;
   auto put = [&](int idx, long e) { ok = ok && compact(w2N + 4L * (((e % N2) + N2) % N2), out + 2L * idx); };
@@ -90,6 +90,15 @@ static int v3_tables_impl(const F *w2N /* [2N][4] */, F *out) {
       }
   }
   for (int k = 0; k < N / 2; k++) put(Gm::tw_fin() + k, k);  // z^k (conj'd in-kernel)
+  if (Gm::LAST16) {  // last inverse pass (radix RK) with z^{-k0} folded in: [RK][L]
+    const int p = P.ni - 1, Q = P.q[p], L = v3::iL(P, p), Sp = N / (L * Q);
+    for (int q = 0; q < Q; q++)
+      for (int k0 = 0; k0 < L; k0++) {
+        // direct (q < 8): conj(u) with u = w_{LQ}^{q k0} z^{k0}; mirror: w_{LQ}^{(Q-q) k0} z^{-k0}
+        const long e = (2 * q < Q) ? (long)k0 * (2L * q * Sp + 1) : (long)k0 * (2L * (Q - q) * Sp - 1);
+        put(Gm::tw_l16() + q * L + k0, e);
+      }
+  }
   return ok ? Gm::tw_total() : -4;
 }
 
@@ -113,23 +122,30 @@ static int v3_tables_impl(const F *w2N /* [2N][4] */, F *out) {
     default: return -4;                             \
   }
 
-template <int M> static int v3_table_size_m() { return v3::G3<M>::tw_total(); }
-int v3_table_entries(int m) { IVM_V3_DISPATCH(v3_table_size_m) }
-
-template <int M> static int v3_tables_m(int prec, const void *w2N, void *out) {
-  return prec == 0 ? v3_tables_impl<double, M>((const double *)w2N, (double *)out)
-                   : v3_tables_impl<float, M>((const float *)w2N, (float *)out);
+template <int M> static int v3_table_size_m(int radix) {
+  return radix == 8 ? v3::G3<M, 8>::tw_total() : v3::G3<M, 16>::tw_total();
 }
-int v3_tables(int m, int prec, const void *w2N, void *out) { IVM_V3_DISPATCH(v3_tables_m, prec, w2N, out) }
+int v3_table_entries(int m, int radix) { IVM_V3_DISPATCH(v3_table_size_m, radix) }
 
-template <typename T, int M>
+template <int M> static int v3_tables_m(int prec, int radix, const void *w2N, void *out) {
+  if (radix == 8)
+    return prec == 0 ? v3_tables_impl<double, M, 8>((const double *)w2N, (double *)out)
+                     : v3_tables_impl<float, M, 8>((const float *)w2N, (float *)out);
+  return prec == 0 ? v3_tables_impl<double, M, 16>((const double *)w2N, (double *)out)
+                   : v3_tables_impl<float, M, 16>((const float *)w2N, (float *)out);
+}
+int v3_tables(int m, int prec, int radix, const void *w2N, void *out) {
+  IVM_V3_DISPATCH(v3_tables_m, prec, radix, w2N, out)
+}
+
+template <typename T, int M, int R>
 static int v3_info_impl(LaunchInfo *li) {
-  using C = v3::Cfg3<T, M>;
+  using C = v3::Cfg3<T, M, R>;
   li->threads = C::THREADS;
   li->smem = C::SMEM;
   li->a_smem = false;
   li->a_bytes_per_cta = C::A_BYTES;
-  auto k = v3::ivm_v3_kernel<T, M>;
+  auto k = v3::ivm_v3_kernel<T, M, R>;
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) != cudaSuccess)
     return -1;
   int nb = 0;
@@ -137,29 +153,31 @@ static int v3_info_impl(LaunchInfo *li) {
   li->blocks_per_sm = nb;
   return 0;
 }
-template <int M> static int v3_info_m(int prec, LaunchInfo *li) {
+template <int M> static int v3_info_m(int prec, int radix, LaunchInfo *li) {
   if constexpr (M > 13 || M < 10) {
     return -4;
   } else {
-    return prec == 0 ? v3_info_impl<double, M>(li) : v3_info_impl<float, M>(li);
+    if (radix == 8) return prec == 0 ? v3_info_impl<double, M, 8>(li) : v3_info_impl<float, M, 8>(li);
+    return prec == 0 ? v3_info_impl<double, M, 16>(li) : v3_info_impl<float, M, 16>(li);
   }
 }
-int v3_info(int prec, int m, LaunchInfo *li) { IVM_V3_DISPATCH(v3_info_m, prec, li) }
+int v3_info(int prec, int m, int radix, LaunchInfo *li) { IVM_V3_DISPATCH(v3_info_m, prec, radix, li) }
 
-template <int M> static int v3_launch_m(int prec, const KParams &kp, int grid, cudaStream_t s) {
+template <typename T, int M, int R> static void v3_go(const KParams &kp, int grid, cudaStream_t s) {
+  using C = v3::Cfg3<T, M, R>;
+  v3::ivm_v3_kernel<T, M, R><<<grid, C::THREADS, C::SMEM, s>>>(kp);
+}
+template <int M> static int v3_launch_m(int prec, int radix, const KParams &kp, int grid, cudaStream_t s) {
   if constexpr (M > 13 || M < 10) {
     return -4;
-  } else if (prec == 0) {
-    using C = v3::Cfg3<double, M>;
-    v3::ivm_v3_kernel<double, M><<<grid, C::THREADS, C::SMEM, s>>>(kp);
   } else {
-    using C = v3::Cfg3<float, M>;
-    v3::ivm_v3_kernel<float, M><<<grid, C::THREADS, C::SMEM, s>>>(kp);
+    if (radix == 8) (prec == 0 ? v3_go<double, M, 8> : v3_go<float, M, 8>)(kp, grid, s);
+    else (prec == 0 ? v3_go<double, M, 16> : v3_go<float, M, 16>)(kp, grid, s);
   }
   return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
 }
-int v3_launch(int prec, int m, const KParams &kp, int grid, cudaStream_t s) {
-  IVM_V3_DISPATCH(v3_launch_m, prec, kp, grid, s)
+int v3_launch(int prec, int m, int radix, const KParams &kp, int grid, cudaStream_t s) {
+  IVM_V3_DISPATCH(v3_launch_m, prec, radix, kp, grid, s)
 }
 
 

@@ -50,49 +50,80 @@ __host__ __device__ constexpr Plan plan(int m) {
   }
 }
 
+// plans of the one-CTA kernel by radix (R = 16: plan(m); R = 8: more passes,
+// half the registers per task, twice the warps per SM)
+__host__ __device__ constexpr Plan plan_cta(int m, int R) {
+  if (R != 8) return plan(m);
+  switch (m) {
+    case 10: return Plan{4, {2, 8, 8, 8, 0, 0}, 3, {8, 8, 8, 0, 0, 0}};
+    case 11: return Plan{5, {2, 2, 8, 8, 8, 0}, 4, {8, 8, 8, 2, 0, 0}};
+    case 12: return Plan{5, {2, 4, 8, 8, 8, 0}, 4, {8, 8, 8, 4, 0, 0}};
+    case 13: return Plan{5, {2, 8, 8, 8, 8, 0}, 4, {8, 8, 8, 8, 0, 0}};
+    default: return plan(m);
+  }
+}
+
 __host__ __device__ constexpr int cmax3(int a, int b) { return a > b ? a : b; }
 __host__ __device__ constexpr int fL(const Plan &P, int p) { return p == 0 ? 1 : fL(P, p - 1) * P.f[p - 1]; }
 __host__ __device__ constexpr int iL(const Plan &P, int p) { return p == 0 ? 1 : iL(P, p - 1) * P.q[p - 1]; }
 
 // row stride with padding so that the lanes of a quarter warp (8 x 16 B) hit
 // distinct 16-byte bank groups when the reading pass has S' < 8 columns per task
-__host__ __device__ constexpr int rstride(int S, int Sread) {
-  return Sread >= 8 ? S : S + (((Sread - S) % 8) + 8) % 8;
-}
+__host__ __device__ constexpr int rstride(int S, int Sread) { return S; }
+// XOR swizzle of the column within groups of 8 (no padding): element (row, col)
+// lives at row * S + (col ^ (row & SW)); used when the reading pass takes fewer
+// than 8 consecutive columns per task, so that a quarter warp's 16-B accesses
+// spread over distinct bank groups
+__host__ __device__ constexpr int swzmask(int S, int Sread) { return Sread >= 8 ? 0 : (S >= 8 ? 7 : S - 1); }
+__host__ __device__ __forceinline__ int sidx(int row, int col, int RS, int SW) { return row * RS + (col ^ (row & SW)); }
 
-template <int M> struct G3 {
-  static constexpr Plan P = plan(M);  // (host-side use; device code calls plan(M))
+template <int M, int R = 16> struct G3 {
+  static constexpr Plan P = plan_cta(M, R);  // (host-side use; device code calls plan_cta(M, R))
   static constexpr int N = 1 << M;
-  static constexpr int THREADS = N / 32 < 32 ? 32 : N / 32;
-  static constexpr int TASKS = N / 32;  // tasks x radix = N/2 per pass
+  static constexpr int THREADS = N / (2 * R) < 32 ? 32 : N / (2 * R);
+  static constexpr int TASKS = N / (2 * R);  // tasks x radix = N/2 per pass
   // forward state after pass p (p >= 1): rows L_p/2, cols S_p
-  __host__ __device__ static constexpr int fS(int p) { return N / fL(plan(M), p); }
+  __host__ __device__ static constexpr int fS(int p) { return N / fL(plan_cta(M, R), p); }
   __host__ __device__ static constexpr int fRS(int p) {  // read by forward pass p (radix f[p])
-    return rstride(fS(p), p < plan(M).nf ? fS(p) / plan(M).f[p] : 1);
+    return rstride(fS(p), p < plan_cta(M, R).nf ? fS(p) / plan_cta(M, R).f[p] : 1);
+  }
+  __host__ __device__ static constexpr int fSW(int p) {
+    return swzmask(fS(p), p < plan_cta(M, R).nf ? fS(p) / plan_cta(M, R).f[p] : 1);
   }
   // inverse state after pass p: rows L_p, cols S_p/2 (S_p = N / L_p)
-  __host__ __device__ static constexpr int iS(int p) { return N / iL(plan(M), p); }
-  __host__ __device__ static constexpr int iRS(int p) { return rstride(iS(p) / 2, p < plan(M).ni ? iS(p) / plan(M).q[p] / 2 : 1); }
+  __host__ __device__ static constexpr int iS(int p) { return N / iL(plan_cta(M, R), p); }
+  __host__ __device__ static constexpr int iRS(int p) { return rstride(iS(p) / 2, p < plan_cta(M, R).ni ? iS(p) / plan_cta(M, R).q[p] / 2 : 1); }
+  __host__ __device__ static constexpr int iSW(int p) { return swzmask(iS(p) / 2, p < plan_cta(M, R).ni ? iS(p) / plan_cta(M, R).q[p] / 2 : 1); }
   __host__ __device__ static constexpr int cap() {
     int c = 0;
-    for (int p = 2; p < plan(M).nf; p++) c = cmax3(c, (fL(plan(M), p) / 2) * fRS(p));
-    for (int p = 1; p < plan(M).ni; p++) c = cmax3(c, iL(plan(M), p) * iRS(p));
+    for (int p = 2; p < plan_cta(M, R).nf; p++) c = cmax3(c, (fL(plan_cta(M, R), p) / 2) * fRS(p));
+    for (int p = 1; p < plan_cta(M, R).ni; p++) c = cmax3(c, iL(plan_cta(M, R), p) * iRS(p));
     return c;
   }
   static constexpr int CAP = cap();
   // twiddle table segment offsets (entries of CI<T>)
   __host__ __device__ static constexpr int tw_fwd(int p) {  // p >= 1: [R-1][L/2]
     int o = 0;
-    for (int k = 1; k < p; k++) o += (plan(M).f[k] - 1) * (fL(plan(M), k) / 2);
+    for (int k = 1; k < p; k++) o += (plan_cta(M, R).f[k] - 1) * (fL(plan_cta(M, R), k) / 2);
     return o;
   }
   __host__ __device__ static constexpr int tw_inv(int p) {  // p >= 1: [Q-1][L]
-    int o = tw_fwd(plan(M).nf);
-    for (int k = 1; k < p; k++) o += (plan(M).q[k] - 1) * iL(plan(M), k);
+    int o = tw_fwd(plan_cta(M, R).nf);
+    for (int k = 1; k < p; k++) o += (plan_cta(M, R).q[k] - 1) * iL(plan_cta(M, R), k);
     return o;
   }
-  __host__ __device__ static constexpr int tw_fin() { return tw_inv(plan(M).ni); }  // [Q_last][L_last]
-  __host__ __device__ static constexpr int tw_total() { return tw_fin() + N / 2; }
+  __host__ __device__ static constexpr int tw_fin() { return tw_inv(plan_cta(M, R).ni); }  // [Q_last][L_last]
+  // last inverse pass of radix 16 with the final twist z^{-k0} folded into its
+  // input twiddles: [16][L_last] (q = 0 included)
+  static constexpr bool LAST16 = plan_cta(M, R).q[plan_cta(M, R).ni - 1] == R;  // last inverse radix = R
+  __host__ __device__ static constexpr int tw_l16() { return tw_fin() + N / 2; }
+  __host__ __device__ static constexpr int LASTL() { return iL(plan_cta(M, R), plan_cta(M, R).ni - 1); }
+  __host__ __device__ static constexpr int tw_total() { return tw_l16() + (LAST16 ? R * LASTL() : 0); }
+  // shared-memory twiddle buffer: the forward last pass table or the folded one
+  __host__ __device__ static constexpr int FLAST_ENT() { return (R - 1) * (fL(plan_cta(M, R), plan_cta(M, R).nf - 1) / 2); }
+  __host__ __device__ static constexpr int TWB_ENT() {
+    return cmax3(FLAST_ENT(), LAST16 ? R * LASTL() : 0);
+  }
 };
 
 // ---------------------------------------------------------------------------
@@ -249,12 +280,12 @@ template <typename T> struct Buf {
 // ---------------------------------------------------------------------------
 // pass 1: G_1[0][v] = x[v] (the trivial radix-2 pass 0), read from HBM;
 // G_2[2r][v] = sum_q w_R^{qr} (w_{4R}^q x[v + S'q]), stored with the mirror.
-template <typename T, int M>
+template <typename T, int M, int RK>
 __device__ __forceinline__ void fwd_first(const uint8_t *__restrict__ dig, int n, Buf<T> st,
                                           const TwC<T> *__restrict__ tw) {
-  using Gm = G3<M>;
-  constexpr int N = Gm::N, R = Gm::P.f[1], L = 2, S = N / 2, Sp = S / R, G = 16 / R;
-  constexpr int RSo = Gm::fRS(2);
+  using Gm = G3<M, RK>;
+  constexpr int N = Gm::N, R = Gm::P.f[1], L = 2, S = N / 2, Sp = S / R, G = RK / R;
+  constexpr int RSo = Gm::fRS(2), SWo = Gm::fSW(2);
   CI<T> v[G][R];
 #pragma unroll
   for (int g = 0; g < G; g++) {
@@ -276,86 +307,22 @@ __device__ __forceinline__ void fwd_first(const uint8_t *__restrict__ dig, int n
       cdft<T, R, false>(v[g]);
 #pragma unroll
       for (int r = 0; r < R; r++) {
-        if (r < R / 2) st.st((L * r) * RSo + nu, v[g][r]);
-        else st.st((L * R - 1 - L * r) * RSo + nu, cconj(v[g][r]));
+        if (r < R / 2) st.st(sidx(L * r, nu, RSo, SWo), v[g][r]);
+        else st.st(sidx(L * R - 1 - L * r, nu, RSo, SWo), cconj(v[g][r]));
       }
     }
   }
 }
 
-// forward pass p >= 2 (in place when DST aliases the state)
-template <typename T, int M, int p>
-__device__ __forceinline__ void fwd_load_compute(Buf<T> st, const TwC<T> *__restrict__ tw,
-                                                 CI<T> (&v)[16 / G3<M>::P.f[p]][G3<M>::P.f[p]],
-                                                 int (&k0s)[16 / G3<M>::P.f[p]],
-                                                 int (&nus)[16 / G3<M>::P.f[p]]) {
-  using Gm = G3<M>;
-  constexpr int N = Gm::N, R = Gm::P.f[p], L = fL(Gm::P, p), S = N / L, Sp = S / R, G = 16 / R;
-  constexpr int RSi = Gm::fRS(p);
-  constexpr int TW = Gm::tw_fwd(p);
-  constexpr int COUNT = (L / 2) * Sp;
-#pragma unroll
-  for (int g = 0; g < G; g++) {
-    const int t = threadIdx.x + g * Gm::THREADS;
-    const int k0 = t / Sp, nu = t % Sp;
-    k0s[g] = (Gm::THREADS * G == COUNT || t < COUNT) ? k0 : -1;
-    nus[g] = nu;
-    if (!(Gm::THREADS * G == COUNT || t < COUNT)) continue;
-#pragma unroll
-    for (int q = 0; q < R; q++) {
-      CI<T> z = st.ld(k0 * RSi + nu + Sp * q);
-      if (q > 0) z = rtmul<T, false>(ldg_twc(tw, TW + (q - 1) * (L / 2) + k0), z);
-      v[g][q] = z;
-    }
-    cdft<T, R, false>(v[g]);
-  }
-}
-
-template <typename T, int M, int p>
-__device__ __forceinline__ void fwd_mid(Buf<T> st, const TwC<T> *__restrict__ tw) {
-  using Gm = G3<M>;
-  constexpr int R = Gm::P.f[p], L = fL(Gm::P, p), G = 16 / R;
-  constexpr int RSo = Gm::fRS(p + 1);
-  CI<T> v[G][R];
-  int k0s[G], nus[G];
-  fwd_load_compute<T, M, p>(st, tw, v, k0s, nus);
-  __syncthreads();
-#pragma unroll
-  for (int g = 0; g < G; g++) {
-    if (k0s[g] < 0) continue;
-#pragma unroll
-    for (int r = 0; r < R; r++) {
-      if (r < R / 2) st.st((k0s[g] + L * r) * RSo + nus[g], v[g][r]);
-      else st.st((L * R - 1 - k0s[g] - L * r) * RSo + nus[g], cconj(v[g][r]));
-    }
-  }
-}
-
-// last forward pass of a: spectrum class k0 (all R values) -> A store [r][k0]
-template <typename T, int M>
-__device__ __forceinline__ void fwd_last_a(Buf<T> st, Buf<T> A, const TwC<T> *__restrict__ tw) {
-  using Gm = G3<M>;
-  constexpr int p = Gm::P.nf - 1, R = Gm::P.f[p], L = fL(Gm::P, p), G = 16 / R;
-  CI<T> v[G][R];
-  int k0s[G], nus[G];
-  fwd_load_compute<T, M, p>(st, tw, v, k0s, nus);
-#pragma unroll
-  for (int g = 0; g < G; g++) {
-    if (k0s[g] < 0) continue;
-#pragma unroll
-    for (int r = 0; r < R; r++) A.st(r * (L / 2) + k0s[g], v[g][r]);
-  }
-}
-
 // inverse pass: loads of E_p[k0][v + S'q] with the mirror (q >= Q/2)
-template <typename T, int M, int p>
+template <typename T, int M, int RK, int p>
 __device__ __forceinline__ void inv_load_compute(Buf<T> st, const TwC<T> *__restrict__ tw,
-                                                 CI<T> (&v)[16 / G3<M>::P.q[p]][G3<M>::P.q[p]],
-                                                 int (&k0s)[16 / G3<M>::P.q[p]],
-                                                 int (&nus)[16 / G3<M>::P.q[p]]) {
-  using Gm = G3<M>;
-  constexpr int N = Gm::N, Q = Gm::P.q[p], L = iL(Gm::P, p), S = N / L, Sp = S / Q, G = 16 / Q;
-  constexpr int H = Sp / 2, RSi = Gm::iRS(p);
+                                                 CI<T> (&v)[RK / G3<M, RK>::P.q[p]][G3<M, RK>::P.q[p]],
+                                                 int (&k0s)[RK / G3<M, RK>::P.q[p]],
+                                                 int (&nus)[RK / G3<M, RK>::P.q[p]]) {
+  using Gm = G3<M, RK>;
+  constexpr int N = Gm::N, Q = Gm::P.q[p], L = iL(Gm::P, p), S = N / L, Sp = S / Q, G = RK / Q;
+  constexpr int H = Sp / 2, RSi = Gm::iRS(p), SWi = Gm::iSW(p);
   constexpr int TW = Gm::tw_inv(p);
   constexpr int COUNT = L * H;
 #pragma unroll
@@ -368,8 +335,8 @@ __device__ __forceinline__ void inv_load_compute(Buf<T> st, const TwC<T> *__rest
 #pragma unroll
     for (int q = 0; q < Q; q++) {
       CI<T> z;
-      if (2 * q < Q) z = st.ld(k0 * RSi + nu + Sp * q);
-      else z = cconj(st.ld(k0 * RSi + (S - 1 - nu - Sp * q)));
+      if (2 * q < Q) z = st.ld(sidx(k0, nu + Sp * q, RSi, SWi));
+      else z = cconj(st.ld(sidx(k0, S - 1 - nu - Sp * q, RSi, SWi)));
       if (q > 0) {
         const TwC<T> w = ldg_twc(tw, TW + (q - 1) * L + k0);
         z = (2 * q < Q) ? rtmul<T, true>(w, z) : rtmul<T, false>(w, z);
@@ -378,24 +345,6 @@ __device__ __forceinline__ void inv_load_compute(Buf<T> st, const TwC<T> *__rest
     }
     cdft<T, Q, true>(v[g]);
   }
-}
-
-template <typename T, int M, int p>
-__device__ __forceinline__ void inv_mid(Buf<T> st, const TwC<T> *__restrict__ tw) {
-  using Gm = G3<M>;
-  constexpr int N = Gm::N, Q = Gm::P.q[p], L = iL(Gm::P, p), G = 16 / Q;
-  constexpr int RSo = Gm::iRS(p + 1);
-  CI<T> v[G][Q];
-  int k0s[G], nus[G];
-  inv_load_compute<T, M, p>(st, tw, v, k0s, nus);
-  __syncthreads();
-#pragma unroll
-  for (int g = 0; g < G; g++) {
-    if (k0s[g] < 0) continue;
-#pragma unroll
-    for (int r = 0; r < Q; r++) st.st((k0s[g] + L * r) * RSo + nus[g], v[g][r]);
-  }
-  (void)N;
 }
 
 // ---------------------------------------------------------------------------
@@ -460,15 +409,27 @@ __device__ __forceinline__ void emit_coeffs(const CI<T> &o, int k, const TwC<T> 
   certify_real(DR<T>::mul_rd(v.il, s), DR<T>::mul_ru(v.ih, s), k + N / 2, n, coef, acc, dump);
 }
 
-template <typename T, int M>
+// folded variant: the input twiddles already carried z^{-k0}; the remaining
+// factor z^{-L r} = conj(w_RATIO^r) (RATIO = 2m/L) is a compile-time constant
+template <typename T, int M, int RATIO>
+__device__ __forceinline__ void emit_fold(const CI<T> &o, int r, int k, int n, int32_t *coef, CertAcc &acc,
+                                          double *dump) {
+  constexpr int N = 1 << M;
+  const CI<T> v = ctw<T, true>(o, r, RATIO);
+  const T s = T(2) / T(N);
+  certify_real(DR<T>::mul_rd(v.rl, s), DR<T>::mul_ru(v.rh, s), k, n, coef, acc, dump);
+  certify_real(DR<T>::mul_rd(v.il, s), DR<T>::mul_ru(v.ih, s), k + N / 2, n, coef, acc, dump);
+}
+
+template <typename T, int M, int RK>
 __device__ __forceinline__ void inv_last(Buf<T> st, const TwC<T> *__restrict__ tw, int n, int32_t *coef,
                                          CertAcc &acc, double *dump) {
-  using Gm = G3<M>;
-  constexpr int p = Gm::P.ni - 1, Q = Gm::P.q[p], L = iL(Gm::P, p), G = 16 / Q;
+  using Gm = G3<M, RK>;
+  constexpr int p = Gm::P.ni - 1, Q = Gm::P.q[p], L = iL(Gm::P, p), G = RK / Q;
   constexpr int TWF = Gm::tw_fin();
   CI<T> v[G][Q];
   int k0s[G], nus[G];
-  inv_load_compute<T, M, p>(st, tw, v, k0s, nus);
+  inv_load_compute<T, M, RK, p>(st, tw, v, k0s, nus);
 #pragma unroll
   for (int g = 0; g < G; g++) {
     if (k0s[g] < 0) continue;
@@ -480,147 +441,196 @@ __device__ __forceinline__ void inv_last(Buf<T> st, const TwC<T> *__restrict__ t
   }
 }
 
-template <typename T, int M, int p>
-__device__ __forceinline__ void run_fwd(Buf<T> st, const TwC<T> *tw) {
-  if constexpr (p < G3<M>::P.nf - 1) {
-    fwd_mid<T, M, p>(st, tw);
-    __syncthreads();
-    run_fwd<T, M, p + 1>(st, tw);
-  }
-}
-
-template <typename T, int M, int p>
-__device__ __forceinline__ void run_inv(Buf<T> st, const TwC<T> *tw) {
-  if constexpr (p < G3<M>::P.ni - 1) {
-    inv_mid<T, M, p>(st, tw);
-    __syncthreads();
-    run_inv<T, M, p + 1>(st, tw);
-  }
-}
-
 // ---------------------------------------------------------------------------
 // runtime-parameterised radix-16 pass bodies: ONE code copy serves every
 // forward pass p >= 2 (and the last / fused one) and every inverse pass, so the
 // straight-line kernel stays small enough for the instruction cache.
 // ---------------------------------------------------------------------------
 struct PassRT {
-  int lgSp, L, RSi, RSo, tw;
+  int lgSp, L, RSi, RSo, SWi, SWo, tw;
+  int sm;    // twiddles read from the shared-memory buffer (index tw relative to it)
+  int fold;  // last inverse pass with the final twist folded in (q = 0 twiddled too)
 };
 
 __host__ __device__ constexpr int ilog2r(int x) { return x <= 1 ? 0 : 1 + ilog2r(x / 2); }
 
-template <int M> struct RT3 {
-  static constexpr int nf = plan(M).nf, ni = plan(M).ni;
+template <int M, int R> struct RT3 {
+  static constexpr int nf = plan_cta(M, R).nf, ni = plan_cta(M, R).ni;
   static constexpr int NFWD = nf - 2;  // forward passes 2 .. nf-1 (all radix 16)
-  static constexpr bool LAST16 = plan(M).q[ni - 1] == 16;
+  static constexpr bool LAST16 = plan_cta(M, R).q[ni - 1] == R;
   static constexpr int NINV = LAST16 ? ni - 1 : ni - 2;  // inverse passes 1 .. via the shared body
   __host__ __device__ static constexpr PassRT fwd(int i) {
-    return PassRT{ilog2r((1 << M) / fL(plan(M), i + 2) / 16), fL(plan(M), i + 2), G3<M>::fRS(i + 2),
-                  (i + 3 < nf) ? G3<M>::fRS(i + 3) : G3<M>::iRS(1), G3<M>::tw_fwd(i + 2)};
+    return PassRT{ilog2r((1 << M) / fL(plan_cta(M, R), i + 2) / R), fL(plan_cta(M, R), i + 2), G3<M, R>::fRS(i + 2),
+                  (i + 3 < nf) ? G3<M, R>::fRS(i + 3) : G3<M, R>::iRS(1), G3<M, R>::fSW(i + 2),
+                  (i + 3 < nf) ? G3<M, R>::fSW(i + 3) : G3<M, R>::iSW(1),
+                  (i == NFWD - 1) ? 0 : G3<M, R>::tw_fwd(i + 2), (i == NFWD - 1) ? 1 : 0, 0};
   }
   __host__ __device__ static constexpr PassRT inv(int i) {
-    return PassRT{ilog2r((1 << M) / iL(plan(M), i + 1) / 16), iL(plan(M), i + 1), G3<M>::iRS(i + 1),
-                  (i + 2 < ni) ? G3<M>::iRS(i + 2) : 0, G3<M>::tw_inv(i + 1)};
+    return PassRT{ilog2r((1 << M) / iL(plan_cta(M, R), i + 1) / R), iL(plan_cta(M, R), i + 1), G3<M, R>::iRS(i + 1),
+                  (i + 2 < ni) ? G3<M, R>::iRS(i + 2) : 0, G3<M, R>::iSW(i + 1), (i + 2 < ni) ? G3<M, R>::iSW(i + 2) : 0,
+                  (LAST16 && i == NINV - 1) ? 0 : G3<M, R>::tw_inv(i + 1), (LAST16 && i == NINV - 1) ? 1 : 0,
+                  (LAST16 && i == NINV - 1) ? 1 : 0};
   }
 };
 
-template <int M>
+template <int M, int R>
 __device__ __forceinline__ PassRT pick_fwd(int i) {
-  static_assert(RT3<M>::NFWD >= 1 && RT3<M>::NFWD <= 3, "forward passes");
-  constexpr PassRT p0 = RT3<M>::fwd(0);
-  constexpr PassRT p1 = RT3<M>::fwd(RT3<M>::NFWD > 1 ? 1 : 0);
-  constexpr PassRT p2 = RT3<M>::fwd(RT3<M>::NFWD > 2 ? 2 : 0);
+  using X = RT3<M, R>;
+  static_assert(X::NFWD >= 1 && X::NFWD <= 3, "forward passes");
+  constexpr PassRT p0 = X::fwd(0);
+  constexpr PassRT p1 = X::fwd(X::NFWD > 1 ? 1 : 0);
+  constexpr PassRT p2 = X::fwd(X::NFWD > 2 ? 2 : 0);
   return i == 0 ? p0 : (i == 1 ? p1 : p2);
 }
-template <int M>
+template <int M, int R>
 __device__ __forceinline__ PassRT pick_inv(int i) {
-  static_assert(RT3<M>::NINV >= 1 && RT3<M>::NINV <= 3, "inverse passes");
-  constexpr PassRT p0 = RT3<M>::inv(0);
-  constexpr PassRT p1 = RT3<M>::inv(RT3<M>::NINV > 1 ? 1 : 0);
-  constexpr PassRT p2 = RT3<M>::inv(RT3<M>::NINV > 2 ? 2 : 0);
+  using X = RT3<M, R>;
+  static_assert(X::NINV >= 1 && X::NINV <= 3, "inverse passes");
+  constexpr PassRT p0 = X::inv(0);
+  constexpr PassRT p1 = X::inv(X::NINV > 1 ? 1 : 0);
+  constexpr PassRT p2 = X::inv(X::NINV > 2 ? 2 : 0);
   return i == 0 ? p0 : (i == 1 ? p1 : p2);
 }
 
 // L1 prefetch of the twiddles a thread will read in a later pass
-template <typename T>
+template <typename T, int R>
 __device__ __forceinline__ void prefetch_tw(const TwC<T> *tw, const PassRT &pp, bool inverse) {
+  if (pp.sm) return;
   const int t = threadIdx.x;
   const int k0 = inverse ? (t >> (pp.lgSp - 1)) : (t >> pp.lgSp);
   const int stride = inverse ? pp.L : (pp.L >> 1);
   const TwC<T> *b = tw + pp.tw + k0;
 #pragma unroll
-  for (int q = 1; q < 16; q++) asm volatile("prefetch.global.L1 [%0];" ::"l"(b + (q - 1) * stride));
+  for (int q = 1; q < R; q++) asm volatile("prefetch.global.L1 [%0];" ::"l"(b + (q - 1) * stride));
 }
 
-// forward: F_p[k0][nu + Sp q] * w_{32L}^{q(2k0+1)} -> 16-point DFT
 template <typename T>
-__device__ __forceinline__ void fwd16(Buf<T> st, const TwC<T> *__restrict__ tw, const PassRT &pp,
-                                      CI<T> (&v)[16], int &k0, int &nu) {
+__device__ __forceinline__ TwC<T> ld_twc(const TwC<T> *p) {  // generic (global or shared)
+  return *p;
+}
+
+// forward: F_p[k0][nu + Sp q] * w_{2LR}^{q(2k0+1)} -> R-point DFT
+template <typename T, int R>
+__device__ __forceinline__ void fwdR(Buf<T> st, const TwC<T> *__restrict__ tw, const TwC<T> *twb,
+                                     const PassRT &pp, CI<T> (&v)[R], int &k0, int &nu) {
   const int t = threadIdx.x, Sp = 1 << pp.lgSp;
   k0 = t >> pp.lgSp;
   nu = t & (Sp - 1);
-  const int base = k0 * pp.RSi + nu, tb = pp.tw + k0, tstride = pp.L >> 1;
+  const int base = k0 * pp.RSi, sw = k0 & pp.SWi, tstride = pp.L >> 1;
+  const TwC<T> *tp = (pp.sm ? twb : tw) + pp.tw + k0;
 #pragma unroll
-  for (int q = 0; q < 16; q++) {
-    CI<T> z = st.ld(base + Sp * q);
-    if (q > 0) z = rtmul<T, false>(ldg_twc(tw, tb + (q - 1) * tstride), z);
+  for (int q = 0; q < R; q++) {
+    CI<T> z = st.ld(base + ((nu + Sp * q) ^ sw));
+    if (q > 0) z = rtmul<T, false>(ld_twc(tp + (q - 1) * tstride), z);
     v[q] = z;
   }
-  cdft<T, 16, false>(v);
+  cdft<T, R, false>(v);
 }
 
-// inverse: E_p[k0][mu] (mirror for q >= 8) * twiddle -> 16-point inverse DFT
-template <typename T>
-__device__ __forceinline__ void inv16(Buf<T> st, const TwC<T> *__restrict__ tw, const PassRT &pp,
-                                      CI<T> (&v)[16], int &k0, int &nu) {
-  const int t = threadIdx.x, Sp = 1 << pp.lgSp, lgH = pp.lgSp - 1, S = 16 * Sp;
+// inverse: E_p[k0][mu] (mirror for q >= R/2) * twiddle -> R-point inverse DFT
+template <typename T, int R>
+__device__ __forceinline__ void invR(Buf<T> st, const TwC<T> *__restrict__ tw, const TwC<T> *twb,
+                                     const PassRT &pp, CI<T> (&v)[R], int &k0, int &nu) {
+  const int t = threadIdx.x, Sp = 1 << pp.lgSp, lgH = pp.lgSp - 1, S = R * Sp;
   k0 = t >> lgH;
   nu = t & ((Sp >> 1) - 1);
-  const int base = k0 * pp.RSi, tb = pp.tw + k0;
+  const int base = k0 * pp.RSi, sw = k0 & pp.SWi;
+  // folded last pass: entries [q][k0] for q = 0..15, else [q-1][k0]
+  const TwC<T> *tp = (pp.sm ? twb : tw) + pp.tw + k0 + (pp.fold ? 0 : -pp.L);
 #pragma unroll
-  for (int q = 0; q < 16; q++) {
+  for (int q = 0; q < R; q++) {
     CI<T> z;
-    if (q < 8) z = st.ld(base + nu + Sp * q);
-    else z = cconj(st.ld(base + (S - 1 - nu - Sp * q)));
-    if (q > 0) {
-      const TwC<T> w = ldg_twc(tw, tb + (q - 1) * pp.L);
-      z = (q < 8) ? rtmul<T, true>(w, z) : rtmul<T, false>(w, z);
+    if (2 * q < R) z = st.ld(base + ((nu + Sp * q) ^ sw));
+    else z = cconj(st.ld(base + ((S - 1 - nu - Sp * q) ^ sw)));
+    if (q > 0 || pp.fold) {
+      const TwC<T> w = ld_twc(tp + q * pp.L);
+      z = (2 * q < R) ? rtmul<T, true>(w, z) : rtmul<T, false>(w, z);
     }
     v[q] = z;
   }
-  cdft<T, 16, true>(v);
+  cdft<T, R, true>(v);
 }
 
-template <typename T, int M> struct Cfg3 {
-  using Gm = G3<M>;
+// ---- 1-D bulk async copy (TMA) of a twiddle table into shared memory ----
+__device__ __forceinline__ void mbar_init(unsigned long long *bar) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst), b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+               "l"(src), "r"(bytes), "r"(b)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phase) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(b), "r"(phase)
+        : "memory");
+  }
+}
+
+template <typename T, int M, int R> struct Cfg3 {
+  using Gm = G3<M, R>;
+  // target warps per SM: 16 for radix 8 (<= 128 registers), 8 for radix 16
+  static constexpr int MINB = (R == 8 ? 512 : 256) / Gm::THREADS < 1 ? 1 : (R == 8 ? 512 : 256) / Gm::THREADS;
   static constexpr int N = Gm::N, THREADS = Gm::THREADS, CAP = Gm::CAP;
   static constexpr size_t E = sizeof(typename V2t<T>::t);
   static constexpr size_t STATE_BYTES = 2 * E * (size_t)CAP;
   static constexpr size_t COEF_BYTES = 4 * (size_t)N;
   static constexpr size_t A_BYTES = 2 * E * (size_t)(N / 2);  // [R][L/2] x (re, im)
-  static constexpr size_t SMEM = STATE_BYTES + COEF_BYTES;
+  static constexpr size_t TWB_BYTES = sizeof(TwC<T>) * (size_t)Gm::TWB_ENT();
+  static constexpr size_t SMEM = STATE_BYTES + COEF_BYTES + TWB_BYTES;
 };
 
-template <typename T, int M>
-__global__ void __launch_bounds__(Cfg3<T, M>::THREADS, 1) ivm_v3_kernel(KParams kp) {
-  using C = Cfg3<T, M>;
-  using Gm = G3<M>;
+template <typename T, int M, int R>
+__global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) ivm_v3_kernel(KParams kp) {
+  using C = Cfg3<T, M, R>;
+  using Gm = G3<M, R>;
   using V = typename V2t<T>::t;
   constexpr int N = C::N;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Cert3 cs;
   Buf<T> st{reinterpret_cast<V *>(smem), reinterpret_cast<V *>(smem) + C::CAP};
   int32_t *coef = reinterpret_cast<int32_t *>(smem + C::STATE_BYTES);
+  TwC<T> *twb = reinterpret_cast<TwC<T> *>(smem + C::STATE_BYTES + C::COEF_BYTES);
+  __shared__ __align__(8) unsigned long long tbar;
   Buf<T> A{reinterpret_cast<V *>(kp.ascratch) + (size_t)blockIdx.x * N, nullptr};
   A.im = A.re + N / 2;
   const TwC<T> *tw = reinterpret_cast<const TwC<T> *>(kp.tw);
   const int n = kp.n;
 
-  constexpr int NFWD = RT3<M>::NFWD, NINV = RT3<M>::NINV;
-  constexpr bool LAST16 = RT3<M>::LAST16;
-  constexpr int RSI1 = Gm::iRS(1), TWF = Gm::tw_fin();
+  constexpr int NFWD = RT3<M, R>::NFWD, NINV = RT3<M, R>::NINV;
+  constexpr bool LAST16 = RT3<M, R>::LAST16;
+  constexpr int RSI1 = Gm::iRS(1), SWI1 = Gm::iSW(1), TWF = Gm::tw_fin();
+  constexpr unsigned FL_BYTES = sizeof(TwC<T>) * Gm::FLAST_ENT();
+  constexpr unsigned L16_BYTES = LAST16 ? sizeof(TwC<T>) * R * Gm::LASTL() : 0;
+  constexpr int RATIO = 2 * N / Gm::LASTL();
+  // shared-memory twiddle buffer: forward-last table (resident unless the
+  // folded inverse table takes its place for the last inverse pass)
+  if (threadIdx.x == 0) mbar_init(&tbar);
+  __syncthreads();
+  if (threadIdx.x == 0 && blockIdx.x < kp.batch) bulk_load(twb, tw + Gm::tw_fwd(Gm::P.nf - 1), FL_BYTES, &tbar);
+  unsigned ph = 0;
+  bool pending = true;
 
   for (int pair = blockIdx.x; pair < kp.batch; pair += gridDim.x) {
+    {  // L2 prefetch of the next pair's digits (read ~one multiplication later)
+      const int nxt = pair + (int)gridDim.x;
+      if (nxt < kp.batch) {
+        for (int off = threadIdx.x * 128; off < n; off += blockDim.x * 128) {
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(kp.a + (size_t)nxt * n + off));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(kp.b + (size_t)nxt * n + off));
+        }
+      }
+    }
     double *dump = nullptr;
     if (kp.dump_slot) {
       const int s = kp.dump_slot[pair];
@@ -628,7 +638,7 @@ __global__ void __launch_bounds__(Cfg3<T, M>::THREADS, 1) ivm_v3_kernel(KParams 
     }
 #pragma unroll 1
     for (int op = 0; op < 2; op++) {
-      fwd_first<T, M>((op == 0 ? kp.a : kp.b) + (size_t)pair * n, n, st, tw);
+      fwd_first<T, M, R>((op == 0 ? kp.a : kp.b) + (size_t)pair * n, n, st, tw);
       if (op == 1 && threadIdx.x == 0) {
         cs.ok = 1;
         cs.first_bad = 0x7fffffff;
@@ -637,57 +647,76 @@ __global__ void __launch_bounds__(Cfg3<T, M>::THREADS, 1) ivm_v3_kernel(KParams 
       __syncthreads();
 #pragma unroll 1
       for (int i = 0; i < NFWD; i++) {
-        const PassRT pp = pick_fwd<M>(i);
-        CI<T> v[16];
+        const PassRT pp = pick_fwd<M, R>(i);
+        CI<T> v[R];
         int k0, nu;
-        if (i + 1 < NFWD) prefetch_tw<T>(tw, pick_fwd<M>(i + 1), false);
-        else if (op == 1) prefetch_tw<T>(tw, pick_inv<M>(0), true);
-        fwd16<T>(st, tw, pp, v, k0, nu);
+        if (i + 1 < NFWD) prefetch_tw<T, R>(tw, pick_fwd<M, R>(i + 1), false);
+        else if (op == 1) prefetch_tw<T, R>(tw, pick_inv<M, R>(0), true);
+        if (pp.sm && pending) {
+          mbar_wait(&tbar, ph);
+          ph ^= 1u;
+          pending = false;
+        }
+        fwdR<T, R>(st, tw, twb, pp, v, k0, nu);
         if (i < NFWD - 1) {  // mid pass: store both halves (mirror conjugated)
           __syncthreads();
 #pragma unroll
-          for (int r = 0; r < 16; r++) {
-            if (r < 8) st.st((k0 + pp.L * r) * pp.RSo + nu, v[r]);
-            else st.st((16 * pp.L - 1 - k0 - pp.L * r) * pp.RSo + nu, cconj(v[r]));
+          for (int r = 0; r < R; r++) {
+            if (2 * r < R) st.st(sidx(k0 + pp.L * r, nu, pp.RSo, pp.SWo), v[r]);
+            else st.st(sidx(R * pp.L - 1 - k0 - pp.L * r, nu, pp.RSo, pp.SWo), cconj(v[r]));
           }
         } else if (op == 0) {  // last pass of a: spectrum class k0 -> A
 #pragma unroll
-          for (int r = 0; r < 16; r++) A.st(r * (pp.L >> 1) + k0, v[r]);
+          for (int r = 0; r < R; r++) A.st(r * (pp.L >> 1) + k0, v[r]);
         } else {  // last pass of b + pointwise + inverse pass 0
 #pragma unroll
-          for (int r = 0; r < 16; r++) v[r] = cmul(A.ld(r * (pp.L >> 1) + k0), v[r]);
-          cdft<T, 16, true>(v);
+          for (int r = 0; r < R; r++) v[r] = cmul(A.ld(r * (pp.L >> 1) + k0), v[r]);
+          cdft<T, R, true>(v);
           __syncthreads();
 #pragma unroll
-          for (int r = 0; r < 16; r++) st.st(r * RSI1 + k0, v[r]);
+          for (int r = 0; r < R; r++) st.st(sidx(r, k0, RSI1, SWI1), v[r]);
         }
         __syncthreads();
+        if (LAST16 && op == 1 && i == NFWD - 1 && threadIdx.x == 0) {
+          bulk_load(twb, tw + Gm::tw_l16(), L16_BYTES, &tbar);  // folded inverse table
+        }
+        if (LAST16 && op == 1 && i == NFWD - 1) pending = true;
       }
     }
     CertAcc acc;
 #pragma unroll 1
     for (int i = 0; i < NINV; i++) {
-      const PassRT pp = pick_inv<M>(i);
-      CI<T> v[16];
+      const PassRT pp = pick_inv<M, R>(i);
+      CI<T> v[R];
       int k0, nu;
-      if (i + 1 < NINV) prefetch_tw<T>(tw, pick_inv<M>(i + 1), true);
-      inv16<T>(st, tw, pp, v, k0, nu);
+      if (i + 1 < NINV) prefetch_tw<T, R>(tw, pick_inv<M, R>(i + 1), true);
+      if (pp.sm && pending) {
+        mbar_wait(&tbar, ph);
+        ph ^= 1u;
+        pending = false;
+      }
+      invR<T, R>(st, tw, twb, pp, v, k0, nu);
       if (!LAST16 || i < NINV - 1) {
         __syncthreads();
 #pragma unroll
-        for (int r = 0; r < 16; r++) st.st((k0 + pp.L * r) * pp.RSo + nu, v[r]);
+        for (int r = 0; r < R; r++) st.st(sidx(k0 + pp.L * r, nu, pp.RSo, pp.SWo), v[r]);
       } else {
 #pragma unroll
-        for (int r = 0; r < 16; r++) {
+        for (int r = 0; r < R; r++) {
           const int k = k0 + pp.L * r;
-          emit_coeffs<T, M>(v[r], k, tw, TWF + k, n, coef, acc, dump);
+          emit_fold<T, M, RATIO>(v[r], r, k, n, coef, acc, dump);
         }
       }
       __syncthreads();
     }
-    if constexpr (!LAST16) inv_last<T, M>(st, tw, n, coef, acc, dump);
+    if constexpr (!LAST16) inv_last<T, M, R>(st, tw, n, coef, acc, dump);
     cert_flush(acc, cs);
     __syncthreads();
+    if (LAST16) {  // restore the forward-last table for the next pair of this CTA
+      if (threadIdx.x == 0 && pair + (int)gridDim.x < kp.batch)
+        bulk_load(twb, tw + Gm::tw_fwd(Gm::P.nf - 1), FL_BYTES, &tbar);
+      pending = true;
+    }
     const bool certified = cs.ok != 0;
     carry_store(coef, n, kp.prod + (size_t)pair * 2 * n, certified, reinterpret_cast<uint16_t *>(smem));
     if (kp.coeffs) {

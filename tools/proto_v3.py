@@ -118,3 +118,10 @@ if __name__ == "__main__":
     check(2048, [2, 4, 16, 16], [16, 16, 4])
     check(4096, [2, 8, 16, 16], [16, 16, 8])
     check(8192, [2, 16, 16, 16], [16, 16, 16])
+
+
+def check_r8():
+    check(8192, [2, 8, 8, 8, 8], [8, 8, 8, 8])
+    check(4096, [2, 4, 8, 8, 8], [8, 8, 8, 4])
+    check(2048, [2, 2, 8, 8, 8], [8, 8, 8, 2])
+    check(1024, [2, 8, 8, 8], [8, 8, 8])
