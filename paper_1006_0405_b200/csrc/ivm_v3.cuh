@@ -172,6 +172,20 @@ __device__ __forceinline__ CI<T> q1mul(T c, T s, const CI<T> &d) {
   return t;
 }
 
+// w = c (1 + i) (c == s, i.e. w_8): the c- and s-selects coincide (4 instead of 8)
+template <typename T>
+__device__ __forceinline__ CI<T> q1mul_eq(T c, const CI<T> &d) {
+  using B = TB<T>;
+  const unsigned nxl = B::sgn(d.rl), nxh = B::sgn(d.rh), nyl = B::sgn(d.il), nyh = B::sgn(d.ih);
+  const T cxl = B::sel(c, nxl), cxh = B::sel(c, 1u - nxh), cyl = B::sel(c, nyl), cyh = B::sel(c, 1u - nyh);
+  CI<T> t;
+  t.rl = DR<T>::fma_rd(-cyh, d.ih, DR<T>::mul_rd(cxl, d.rl));
+  t.rh = DR<T>::fma_ru(-cyl, d.il, DR<T>::mul_ru(cxh, d.rh));
+  t.il = DR<T>::fma_rd(cxl, d.rl, DR<T>::mul_rd(cyl, d.il));
+  t.ih = DR<T>::fma_ru(cxh, d.rh, DR<T>::mul_ru(cyh, d.ih));
+  return t;
+}
+
 // k ? i*t : t  (exact; i*t = (-t.im, t.re))
 template <typename T>
 __device__ __forceinline__ CI<T> rot_if(const CI<T> &t, unsigned k) {
@@ -182,13 +196,19 @@ __device__ __forceinline__ CI<T> rot_if(const CI<T> &t, unsigned k) {
 
 // runtime table twiddle (upper half plane, compact + rotation flag) times d;
 // CONJ: conj(w) * d = conj(w * conj(d))
-template <typename T, bool CONJ>
+template <typename T, bool CONJ, bool MAYROT = true>
 __device__ __forceinline__ CI<T> rtmul(const TwC<T> &w, const CI<T> &d) {
   using B = TB<T>;
-  const unsigned k = B::sgn(w.s);
-  const T s = B::absb(w.s);
-  if (CONJ) return cconj(rot_if(q1mul(w.c, s, cconj(d)), k));
-  return rot_if(q1mul(w.c, s, d), k);
+  if constexpr (!MAYROT) {  // the table guarantees k = 0 (angle < pi/2) and s >= 0
+    CI<T> t = q1mul(w.c, w.s, CONJ ? cconj(d) : d);
+    return CONJ ? cconj(t) : t;
+  } else {
+    const unsigned k = B::sgn(w.s);
+    const T s = B::absb(w.s);
+    CI<T> t = q1mul(w.c, s, CONJ ? cconj(d) : d);
+    t = rot_if(t, k);
+    return CONJ ? cconj(t) : t;
+  }
 }
 
 template <typename T>
@@ -219,11 +239,15 @@ __device__ __forceinline__ CI<T> ctw(const CI<T> &o, int j, int M) {
   if (j == 0) return o;
   if (4 * j == M) return INV ? mul_mi(o) : mul_i(o);
   if (4 * j < M) {  // first quadrant
-    const TwC<T> w = cw64<T>(j * (64 / M));
+    const int e = j * (64 / M);
+    const TwC<T> w = cw64<T>(e);
+    if (e == 8) return INV ? cconj(q1mul_eq(w.c, cconj(o))) : q1mul_eq(w.c, o);  // w_8
     return INV ? cconj(q1mul(w.c, w.s, cconj(o))) : q1mul(w.c, w.s, o);
   }
   // second quadrant: w = i * w', w' = w_M^{j - M/4}
-  const TwC<T> w = cw64<T>((j - M / 4) * (64 / M));
+  const int e = (j - M / 4) * (64 / M);
+  const TwC<T> w = cw64<T>(e);
+  if (e == 8) return INV ? mul_mi(cconj(q1mul_eq(w.c, cconj(o)))) : mul_i(q1mul_eq(w.c, o));
   return INV ? mul_mi(cconj(q1mul(w.c, w.s, cconj(o)))) : mul_i(q1mul(w.c, w.s, o));
 }
 
@@ -521,14 +545,18 @@ __device__ __forceinline__ void fwdR(Buf<T> st, const TwC<T> *__restrict__ tw, c
 #pragma unroll
   for (int q = 0; q < R; q++) {
     CI<T> z = st.ld(base + ((nu + Sp * q) ^ sw));
-    if (q > 0) z = rtmul<T, false>(ld_twc(tp + (q - 1) * tstride), z);
+    // angle of w_{2LR}^{q(2k0+1)} < q pi / R: no quadrant rotation for q <= R/2
+    if (q > 0) {
+      const TwC<T> w = ld_twc(tp + (q - 1) * tstride);
+      z = (2 * q <= R) ? rtmul<T, false, false>(w, z) : rtmul<T, false, true>(w, z);
+    }
     v[q] = z;
   }
   cdft<T, R, false>(v);
 }
 
 // inverse: E_p[k0][mu] (mirror for q >= R/2) * twiddle -> R-point inverse DFT
-template <typename T, int R>
+template <typename T, int R, bool FOLD>
 __device__ __forceinline__ void invR(Buf<T> st, const TwC<T> *__restrict__ tw, const TwC<T> *twb,
                                      const PassRT &pp, CI<T> (&v)[R], int &k0, int &nu) {
   const int t = threadIdx.x, Sp = 1 << pp.lgSp, lgH = pp.lgSp - 1, S = R * Sp;
@@ -536,15 +564,19 @@ __device__ __forceinline__ void invR(Buf<T> st, const TwC<T> *__restrict__ tw, c
   nu = t & ((Sp >> 1) - 1);
   const int base = k0 * pp.RSi, sw = k0 & pp.SWi;
   // folded last pass: entries [q][k0] for q = 0..15, else [q-1][k0]
-  const TwC<T> *tp = (pp.sm ? twb : tw) + pp.tw + k0 + (pp.fold ? 0 : -pp.L);
+  const TwC<T> *tp = (pp.sm ? twb : tw) + pp.tw + k0 + (FOLD ? 0 : -pp.L);
 #pragma unroll
   for (int q = 0; q < R; q++) {
     CI<T> z;
     if (2 * q < R) z = st.ld(base + ((nu + Sp * q) ^ sw));
     else z = cconj(st.ld(base + ((S - 1 - nu - Sp * q) ^ sw)));
-    if (q > 0 || pp.fold) {
+    if (q > 0 || FOLD) {
       const TwC<T> w = ld_twc(tp + q * pp.L);
-      z = (2 * q < R) ? rtmul<T, true>(w, z) : rtmul<T, false>(w, z);
+      // unfolded: angle of w_{LQ}^{q' k0} < q' 2pi / Q (q' = min(q, Q-q) <= Q/2): no
+      // rotation unless q' > Q/4
+      const int qq = (2 * q < R) ? q : R - q;
+      if (2 * q < R) z = (FOLD || 4 * qq > R) ? rtmul<T, true, true>(w, z) : rtmul<T, true, false>(w, z);
+      else z = (FOLD || 4 * qq > R) ? rtmul<T, false, true>(w, z) : rtmul<T, false, false>(w, z);
     }
     v[q] = z;
   }
@@ -695,7 +727,8 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
         ph ^= 1u;
         pending = false;
       }
-      invR<T, R>(st, tw, twb, pp, v, k0, nu);
+      if (LAST16 && i == NINV - 1) invR<T, R, true>(st, tw, twb, pp, v, k0, nu);
+      else invR<T, R, false>(st, tw, twb, pp, v, k0, nu);
       if (!LAST16 || i < NINV - 1) {
         __syncthreads();
 #pragma unroll
