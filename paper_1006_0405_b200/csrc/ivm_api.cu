@@ -25,7 +25,7 @@ struct ivm_ctx {
   std::map<std::pair<int, int>, ivm::LaunchInfo> info;
   std::map<std::pair<int, int>, ivm::LaunchInfo> info3;
   bool force_v1 = false;
-  int radix = 8;  // radix of the one-CTA kernel (IVM_RADIX=16 for the register-heavy variant)
+  int radix = 8;  // radix of the one-CTA kernel
   void *ascratch = nullptr;
   size_t ascratch_bytes = 0;
   int32_t *slot = nullptr;
@@ -114,8 +114,6 @@ int ivm_create(ivm_ctx_t *ctx, int device) {
   }
   const char *kv = getenv("IVM_KERNEL");
   c->force_v1 = kv && strcmp(kv, "v1") == 0;
-  const char *rv = getenv("IVM_RADIX");
-  if (rv && strcmp(rv, "16") == 0) c->radix = 16;
   c->consts = true;
   *ctx = c;
   return IVM_OK;

@@ -157,8 +157,8 @@ template <int M> static int v3_info_m(int prec, int radix, LaunchInfo *li) {
   if constexpr (M > 13 || M < 10) {
     return -4;
   } else {
-    if (radix == 8) return prec == 0 ? v3_info_impl<double, M, 8>(li) : v3_info_impl<float, M, 8>(li);
-    return prec == 0 ? v3_info_impl<double, M, 16>(li) : v3_info_impl<float, M, 16>(li);
+    if (radix != 8) return -4;  // the one-CTA kernel is radix 8 only
+    return prec == 0 ? v3_info_impl<double, M, 8>(li) : v3_info_impl<float, M, 8>(li);
   }
 }
 int v3_info(int prec, int m, int radix, LaunchInfo *li) { IVM_V3_DISPATCH(v3_info_m, prec, radix, li) }
@@ -171,8 +171,8 @@ template <int M> static int v3_launch_m(int prec, int radix, const KParams &kp, 
   if constexpr (M > 13 || M < 10) {
     return -4;
   } else {
-    if (radix == 8) (prec == 0 ? v3_go<double, M, 8> : v3_go<float, M, 8>)(kp, grid, s);
-    else (prec == 0 ? v3_go<double, M, 16> : v3_go<float, M, 16>)(kp, grid, s);
+    if (radix != 8) return -4;
+    (prec == 0 ? v3_go<double, M, 8> : v3_go<float, M, 8>)(kp, grid, s);
   }
   return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
 }

@@ -124,6 +124,13 @@ template <int M, int R = 16> struct G3 {
   __host__ __device__ static constexpr int TWB_ENT() {
     return cmax3(FLAST_ENT(), LAST16 ? R * LASTL() : 0);
   }
+  // resident small tables (shared memory, loaded once per CTA): the forward
+  // mid passes 2 .. nf-2 and the inverse mid passes 1 .. ni-2
+  __host__ __device__ static constexpr int SMF_BEGIN() { return tw_fwd(2); }
+  __host__ __device__ static constexpr int SMF_ENT() { return tw_fwd(plan_cta(M, R).nf - 1) - tw_fwd(2); }
+  __host__ __device__ static constexpr int SMI_BEGIN() { return tw_inv(1); }
+  __host__ __device__ static constexpr int SMI_ENT() { return tw_inv(plan_cta(M, R).ni - 1) - tw_inv(1); }
+  __host__ __device__ static constexpr int SM_ENT() { return TWB_ENT() + SMF_ENT() + SMI_ENT(); }
 };
 
 // ---------------------------------------------------------------------------
@@ -454,6 +461,7 @@ __device__ __forceinline__ void inv_last(Buf<T> st, const TwC<T> *__restrict__ t
   CI<T> v[G][Q];
   int k0s[G], nus[G];
   inv_load_compute<T, M, RK, p>(st, tw, v, k0s, nus);
+  __syncthreads();  // every input loaded: the coefficients may overwrite the state
 #pragma unroll
   for (int g = 0; g < G; g++) {
     if (k0s[g] < 0) continue;
@@ -471,29 +479,34 @@ __device__ __forceinline__ void inv_last(Buf<T> st, const TwC<T> *__restrict__ t
 // straight-line kernel stays small enough for the instruction cache.
 // ---------------------------------------------------------------------------
 struct PassRT {
-  int lgSp, L, RSi, RSo, SWi, SWo, tw;
-  int sm;    // twiddles read from the shared-memory buffer (index tw relative to it)
+  int lgSp, L, RSi, RSo, SWi, SWo;
+  int tw;    // offset of the pass table in the shared-memory twiddle area
+  int big;   // table lives in the swapped big buffer (forward-last / folded)
   int fold;  // last inverse pass with the final twist folded in (q = 0 twiddled too)
 };
 
 __host__ __device__ constexpr int ilog2r(int x) { return x <= 1 ? 0 : 1 + ilog2r(x / 2); }
 
+// shared-memory twiddle area: [TWB_ENT big buffer][forward mid tables][inverse mid tables]
 template <int M, int R> struct RT3 {
+  using Gm = G3<M, R>;
   static constexpr int nf = plan_cta(M, R).nf, ni = plan_cta(M, R).ni;
-  static constexpr int NFWD = nf - 2;  // forward passes 2 .. nf-1 (all radix 16)
+  static constexpr int NFWD = nf - 2;  // forward passes 2 .. nf-1
   static constexpr bool LAST16 = plan_cta(M, R).q[ni - 1] == R;
   static constexpr int NINV = LAST16 ? ni - 1 : ni - 2;  // inverse passes 1 .. via the shared body
   __host__ __device__ static constexpr PassRT fwd(int i) {
-    return PassRT{ilog2r((1 << M) / fL(plan_cta(M, R), i + 2) / R), fL(plan_cta(M, R), i + 2), G3<M, R>::fRS(i + 2),
-                  (i + 3 < nf) ? G3<M, R>::fRS(i + 3) : G3<M, R>::iRS(1), G3<M, R>::fSW(i + 2),
-                  (i + 3 < nf) ? G3<M, R>::fSW(i + 3) : G3<M, R>::iSW(1),
-                  (i == NFWD - 1) ? 0 : G3<M, R>::tw_fwd(i + 2), (i == NFWD - 1) ? 1 : 0, 0};
+    return PassRT{ilog2r((1 << M) / fL(plan_cta(M, R), i + 2) / R), fL(plan_cta(M, R), i + 2), Gm::fRS(i + 2),
+                  (i + 3 < nf) ? Gm::fRS(i + 3) : Gm::iRS(1), Gm::fSW(i + 2),
+                  (i + 3 < nf) ? Gm::fSW(i + 3) : Gm::iSW(1),
+                  (i == NFWD - 1) ? 0 : Gm::TWB_ENT() + Gm::tw_fwd(i + 2) - Gm::SMF_BEGIN(), (i == NFWD - 1) ? 1 : 0,
+                  0};
   }
   __host__ __device__ static constexpr PassRT inv(int i) {
-    return PassRT{ilog2r((1 << M) / iL(plan_cta(M, R), i + 1) / R), iL(plan_cta(M, R), i + 1), G3<M, R>::iRS(i + 1),
-                  (i + 2 < ni) ? G3<M, R>::iRS(i + 2) : 0, G3<M, R>::iSW(i + 1), (i + 2 < ni) ? G3<M, R>::iSW(i + 2) : 0,
-                  (LAST16 && i == NINV - 1) ? 0 : G3<M, R>::tw_inv(i + 1), (LAST16 && i == NINV - 1) ? 1 : 0,
-                  (LAST16 && i == NINV - 1) ? 1 : 0};
+    return PassRT{ilog2r((1 << M) / iL(plan_cta(M, R), i + 1) / R), iL(plan_cta(M, R), i + 1), Gm::iRS(i + 1),
+                  (i + 2 < ni) ? Gm::iRS(i + 2) : 0, Gm::iSW(i + 1), (i + 2 < ni) ? Gm::iSW(i + 2) : 0,
+                  (LAST16 && i == NINV - 1) ? 0
+                                            : Gm::TWB_ENT() + Gm::SMF_ENT() + Gm::tw_inv(i + 1) - Gm::SMI_BEGIN(),
+                  (LAST16 && i == NINV - 1) ? 1 : 0, (LAST16 && i == NINV - 1) ? 1 : 0};
   }
 };
 
@@ -516,38 +529,21 @@ __device__ __forceinline__ PassRT pick_inv(int i) {
   return i == 0 ? p0 : (i == 1 ? p1 : p2);
 }
 
-// L1 prefetch of the twiddles a thread will read in a later pass
-template <typename T, int R>
-__device__ __forceinline__ void prefetch_tw(const TwC<T> *tw, const PassRT &pp, bool inverse) {
-  if (pp.sm) return;
-  const int t = threadIdx.x;
-  const int k0 = inverse ? (t >> (pp.lgSp - 1)) : (t >> pp.lgSp);
-  const int stride = inverse ? pp.L : (pp.L >> 1);
-  const TwC<T> *b = tw + pp.tw + k0;
-#pragma unroll
-  for (int q = 1; q < R; q++) asm volatile("prefetch.global.L1 [%0];" ::"l"(b + (q - 1) * stride));
-}
-
-template <typename T>
-__device__ __forceinline__ TwC<T> ld_twc(const TwC<T> *p) {  // generic (global or shared)
-  return *p;
-}
-
 // forward: F_p[k0][nu + Sp q] * w_{2LR}^{q(2k0+1)} -> R-point DFT
 template <typename T, int R>
-__device__ __forceinline__ void fwdR(Buf<T> st, const TwC<T> *__restrict__ tw, const TwC<T> *twb,
-                                     const PassRT &pp, CI<T> (&v)[R], int &k0, int &nu) {
+__device__ __forceinline__ void fwdR(Buf<T> st, const TwC<T> *twb, const PassRT &pp, CI<T> (&v)[R], int &k0,
+                                     int &nu) {
   const int t = threadIdx.x, Sp = 1 << pp.lgSp;
   k0 = t >> pp.lgSp;
   nu = t & (Sp - 1);
   const int base = k0 * pp.RSi, sw = k0 & pp.SWi, tstride = pp.L >> 1;
-  const TwC<T> *tp = (pp.sm ? twb : tw) + pp.tw + k0;
+  const TwC<T> *tp = twb + pp.tw + k0;
 #pragma unroll
   for (int q = 0; q < R; q++) {
     CI<T> z = st.ld(base + ((nu + Sp * q) ^ sw));
     // angle of w_{2LR}^{q(2k0+1)} < q pi / R: no quadrant rotation for q <= R/2
     if (q > 0) {
-      const TwC<T> w = ld_twc(tp + (q - 1) * tstride);
+      const TwC<T> w = tp[(q - 1) * tstride];
       z = (2 * q <= R) ? rtmul<T, false, false>(w, z) : rtmul<T, false, true>(w, z);
     }
     v[q] = z;
@@ -557,21 +553,21 @@ __device__ __forceinline__ void fwdR(Buf<T> st, const TwC<T> *__restrict__ tw, c
 
 // inverse: E_p[k0][mu] (mirror for q >= R/2) * twiddle -> R-point inverse DFT
 template <typename T, int R, bool FOLD>
-__device__ __forceinline__ void invR(Buf<T> st, const TwC<T> *__restrict__ tw, const TwC<T> *twb,
-                                     const PassRT &pp, CI<T> (&v)[R], int &k0, int &nu) {
+__device__ __forceinline__ void invR(Buf<T> st, const TwC<T> *twb, const PassRT &pp, CI<T> (&v)[R], int &k0,
+                                     int &nu) {
   const int t = threadIdx.x, Sp = 1 << pp.lgSp, lgH = pp.lgSp - 1, S = R * Sp;
   k0 = t >> lgH;
   nu = t & ((Sp >> 1) - 1);
   const int base = k0 * pp.RSi, sw = k0 & pp.SWi;
   // folded last pass: entries [q][k0] for q = 0..15, else [q-1][k0]
-  const TwC<T> *tp = (pp.sm ? twb : tw) + pp.tw + k0 + (FOLD ? 0 : -pp.L);
+  const TwC<T> *tp = twb + pp.tw + k0 + (FOLD ? 0 : -pp.L);
 #pragma unroll
   for (int q = 0; q < R; q++) {
     CI<T> z;
     if (2 * q < R) z = st.ld(base + ((nu + Sp * q) ^ sw));
     else z = cconj(st.ld(base + ((S - 1 - nu - Sp * q) ^ sw)));
     if (q > 0 || FOLD) {
-      const TwC<T> w = ld_twc(tp + q * pp.L);
+      const TwC<T> w = tp[q * pp.L];
       // unfolded: angle of w_{LQ}^{q' k0} < q' 2pi / Q (q' = min(q, Q-q) <= Q/2): no
       // rotation unless q' > Q/4
       const int qq = (2 * q < R) ? q : R - q;
@@ -583,16 +579,22 @@ __device__ __forceinline__ void invR(Buf<T> st, const TwC<T> *__restrict__ tw, c
   cdft<T, R, true>(v);
 }
 
-// ---- 1-D bulk async copy (TMA) of a twiddle table into shared memory ----
+// ---- 1-D bulk async copies (TMA engine) into shared memory, mbarrier-tracked ----
 __device__ __forceinline__ void mbar_init(unsigned long long *bar) {
   const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a));
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
-__device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst), b = (unsigned)__cvta_generic_to_shared(bar);
+// one arrival announcing `bytes` of transactions; precedes the copies it covers
+__device__ __forceinline__ void mbar_expect(unsigned long long *bar, unsigned bytes) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  // generic-proxy accesses of the destination (ordered before this by a CTA
+  // barrier) complete before the async proxy overwrites it
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_copy(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst), b = (unsigned)__cvta_generic_to_shared(bar);
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
                "l"(src), "r"(bytes), "r"(b)
                : "memory");
@@ -609,17 +611,27 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phas
   }
 }
 
+// shared memory of the one-CTA kernel (bytes):
+//   [state: 2 planes x CAP]  (the int32 coefficients and the carry scratch alias
+//                             it once the last inverse pass has loaded its inputs)
+//   [twiddles: big buffer (forward-last table <-> folded inverse table) + the
+//              resident mid-pass tables]
+//   [digits: a | b of the current pair, staged by a bulk copy one pair ahead]
 template <typename T, int M, int R> struct Cfg3 {
   using Gm = G3<M, R>;
-  // target warps per SM: 16 for radix 8 (<= 128 registers), 8 for radix 16
-  static constexpr int MINB = (R == 8 ? 512 : 256) / Gm::THREADS < 1 ? 1 : (R == 8 ? 512 : 256) / Gm::THREADS;
+  static_assert(R == 8, "one-CTA kernel: radix 8 (<= 128 registers, 16 warps per SM)");
   static constexpr int N = Gm::N, THREADS = Gm::THREADS, CAP = Gm::CAP;
+  static constexpr int MINB = 512 / THREADS < 1 ? 1 : 512 / THREADS;
   static constexpr size_t E = sizeof(typename V2t<T>::t);
   static constexpr size_t STATE_BYTES = 2 * E * (size_t)CAP;
   static constexpr size_t COEF_BYTES = 4 * (size_t)N;
+  static constexpr size_t UBUF_BYTES = 2 * ((size_t)N + 8);
   static constexpr size_t A_BYTES = 2 * E * (size_t)(N / 2);  // [R][L/2] x (re, im)
-  static constexpr size_t TWB_BYTES = sizeof(TwC<T>) * (size_t)Gm::TWB_ENT();
-  static constexpr size_t SMEM = STATE_BYTES + COEF_BYTES + TWB_BYTES;
+  static constexpr size_t TW_BYTES = sizeof(TwC<T>) * (size_t)Gm::SM_ENT();
+  static constexpr size_t DIG_BYTES = (size_t)N;  // 2n <= N
+  static constexpr size_t SMEM = STATE_BYTES + TW_BYTES + DIG_BYTES;
+  static_assert(STATE_BYTES >= COEF_BYTES + UBUF_BYTES, "coefficients + carry scratch alias the state");
+  static_assert(SMEM <= 227 * 1024, "shared memory");
 };
 
 template <typename T, int M, int R>
@@ -630,10 +642,12 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
   constexpr int N = C::N;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Cert3 cs;
+  __shared__ __align__(8) unsigned long long tbar, dbar;
   Buf<T> st{reinterpret_cast<V *>(smem), reinterpret_cast<V *>(smem) + C::CAP};
-  int32_t *coef = reinterpret_cast<int32_t *>(smem + C::STATE_BYTES);
-  TwC<T> *twb = reinterpret_cast<TwC<T> *>(smem + C::STATE_BYTES + C::COEF_BYTES);
-  __shared__ __align__(8) unsigned long long tbar;
+  int32_t *coef = reinterpret_cast<int32_t *>(smem);  // aliases the state (see Cfg3)
+  uint16_t *ubuf = reinterpret_cast<uint16_t *>(smem + C::COEF_BYTES);
+  TwC<T> *twb = reinterpret_cast<TwC<T> *>(smem + C::STATE_BYTES);
+  uint8_t *sdig = smem + C::STATE_BYTES + C::TW_BYTES;
   Buf<T> A{reinterpret_cast<V *>(kp.ascratch) + (size_t)blockIdx.x * N, nullptr};
   A.im = A.re + N / 2;
   const TwC<T> *tw = reinterpret_cast<const TwC<T> *>(kp.tw);
@@ -641,27 +655,44 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
 
   constexpr int NFWD = RT3<M, R>::NFWD, NINV = RT3<M, R>::NINV;
   constexpr bool LAST16 = RT3<M, R>::LAST16;
-  constexpr int RSI1 = Gm::iRS(1), SWI1 = Gm::iSW(1), TWF = Gm::tw_fin();
+  constexpr int RSI1 = Gm::iRS(1), SWI1 = Gm::iSW(1);
   constexpr unsigned FL_BYTES = sizeof(TwC<T>) * Gm::FLAST_ENT();
   constexpr unsigned L16_BYTES = LAST16 ? sizeof(TwC<T>) * R * Gm::LASTL() : 0;
+  constexpr unsigned SMF_BYTES = sizeof(TwC<T>) * Gm::SMF_ENT(), SMI_BYTES = sizeof(TwC<T>) * Gm::SMI_ENT();
   constexpr int RATIO = 2 * N / Gm::LASTL();
-  // shared-memory twiddle buffer: forward-last table (resident unless the
-  // folded inverse table takes its place for the last inverse pass)
-  if (threadIdx.x == 0) mbar_init(&tbar);
+  // digits staged by bulk copies when every row is 16-byte aligned
+  const bool staged =
+      (n % 16 == 0) && ((reinterpret_cast<uintptr_t>(kp.a) | reinterpret_cast<uintptr_t>(kp.b)) % 16 == 0);
+  if (threadIdx.x == 0) {
+    mbar_init(&tbar);
+    mbar_init(&dbar);
+  }
   __syncthreads();
-  if (threadIdx.x == 0 && blockIdx.x < kp.batch) bulk_load(twb, tw + Gm::tw_fwd(Gm::P.nf - 1), FL_BYTES, &tbar);
-  unsigned ph = 0;
+  if (threadIdx.x == 0 && blockIdx.x < kp.batch) {
+    mbar_expect(&tbar, FL_BYTES + SMF_BYTES + SMI_BYTES);
+    bulk_copy(twb, tw + Gm::tw_fwd(Gm::P.nf - 1), FL_BYTES, &tbar);
+    if (SMF_BYTES) bulk_copy(twb + Gm::TWB_ENT(), tw + Gm::SMF_BEGIN(), SMF_BYTES, &tbar);
+    if (SMI_BYTES) bulk_copy(twb + Gm::TWB_ENT() + Gm::SMF_ENT(), tw + Gm::SMI_BEGIN(), SMI_BYTES, &tbar);
+    if (staged) {
+      mbar_expect(&dbar, 2u * n);
+      bulk_copy(sdig, kp.a + (size_t)blockIdx.x * n, n, &dbar);
+      bulk_copy(sdig + n, kp.b + (size_t)blockIdx.x * n, n, &dbar);
+    }
+  }
+  unsigned ph = 0, dph = 0;
   bool pending = true;
 
   for (int pair = blockIdx.x; pair < kp.batch; pair += gridDim.x) {
-    {  // L2 prefetch of the next pair's digits (read ~one multiplication later)
-      const int nxt = pair + (int)gridDim.x;
-      if (nxt < kp.batch) {
-        for (int off = threadIdx.x * 128; off < n; off += blockDim.x * 128) {
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(kp.a + (size_t)nxt * n + off));
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(kp.b + (size_t)nxt * n + off));
-        }
+    const int nxt = pair + (int)gridDim.x;
+    if (!staged && nxt < kp.batch) {  // L2 prefetch of the next pair's digits
+      for (int off = threadIdx.x * 128; off < n; off += blockDim.x * 128) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(kp.a + (size_t)nxt * n + off));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(kp.b + (size_t)nxt * n + off));
       }
+    }
+    if (staged) {
+      mbar_wait(&dbar, dph);
+      dph ^= 1u;
     }
     double *dump = nullptr;
     if (kp.dump_slot) {
@@ -670,26 +701,30 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
     }
 #pragma unroll 1
     for (int op = 0; op < 2; op++) {
-      fwd_first<T, M, R>((op == 0 ? kp.a : kp.b) + (size_t)pair * n, n, st, tw);
+      const uint8_t *dig = staged ? sdig + op * n : (op == 0 ? kp.a : kp.b) + (size_t)pair * n;
+      fwd_first<T, M, R>(dig, n, st, tw);
       if (op == 1 && threadIdx.x == 0) {
         cs.ok = 1;
         cs.first_bad = 0x7fffffff;
         cs.maxrad = 0ull;
       }
       __syncthreads();
+      if (op == 1 && staged && threadIdx.x == 0 && nxt < kp.batch) {  // digits of the next pair
+        mbar_expect(&dbar, 2u * n);
+        bulk_copy(sdig, kp.a + (size_t)nxt * n, n, &dbar);
+        bulk_copy(sdig + n, kp.b + (size_t)nxt * n, n, &dbar);
+      }
 #pragma unroll 1
       for (int i = 0; i < NFWD; i++) {
         const PassRT pp = pick_fwd<M, R>(i);
         CI<T> v[R];
         int k0, nu;
-        if (i + 1 < NFWD) prefetch_tw<T, R>(tw, pick_fwd<M, R>(i + 1), false);
-        else if (op == 1) prefetch_tw<T, R>(tw, pick_inv<M, R>(0), true);
-        if (pp.sm && pending) {
+        if (pp.big && pending) {
           mbar_wait(&tbar, ph);
           ph ^= 1u;
           pending = false;
         }
-        fwdR<T, R>(st, tw, twb, pp, v, k0, nu);
+        fwdR<T, R>(st, twb, pp, v, k0, nu);
         if (i < NFWD - 1) {  // mid pass: store both halves (mirror conjugated)
           __syncthreads();
 #pragma unroll
@@ -709,10 +744,13 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
           for (int r = 0; r < R; r++) st.st(sidx(r, k0, RSI1, SWI1), v[r]);
         }
         __syncthreads();
-        if (LAST16 && op == 1 && i == NFWD - 1 && threadIdx.x == 0) {
-          bulk_load(twb, tw + Gm::tw_l16(), L16_BYTES, &tbar);  // folded inverse table
+        if (LAST16 && op == 1 && i == NFWD - 1) {
+          if (threadIdx.x == 0) {  // the folded inverse table replaces the forward-last one
+            mbar_expect(&tbar, L16_BYTES);
+            bulk_copy(twb, tw + Gm::tw_l16(), L16_BYTES, &tbar);
+          }
+          pending = true;
         }
-        if (LAST16 && op == 1 && i == NFWD - 1) pending = true;
       }
     }
     CertAcc acc;
@@ -721,24 +759,21 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
       const PassRT pp = pick_inv<M, R>(i);
       CI<T> v[R];
       int k0, nu;
-      if (i + 1 < NINV) prefetch_tw<T, R>(tw, pick_inv<M, R>(i + 1), true);
-      if (pp.sm && pending) {
+      if (pp.big && pending) {
         mbar_wait(&tbar, ph);
         ph ^= 1u;
         pending = false;
       }
-      if (LAST16 && i == NINV - 1) invR<T, R, true>(st, tw, twb, pp, v, k0, nu);
-      else invR<T, R, false>(st, tw, twb, pp, v, k0, nu);
-      if (!LAST16 || i < NINV - 1) {
+      if (LAST16 && i == NINV - 1) {
+        invR<T, R, true>(st, twb, pp, v, k0, nu);
+        __syncthreads();  // every input loaded: the coefficients may overwrite the state
+#pragma unroll
+        for (int r = 0; r < R; r++) emit_fold<T, M, RATIO>(v[r], r, k0 + pp.L * r, n, coef, acc, dump);
+      } else {
+        invR<T, R, false>(st, twb, pp, v, k0, nu);
         __syncthreads();
 #pragma unroll
         for (int r = 0; r < R; r++) st.st(sidx(k0 + pp.L * r, nu, pp.RSo, pp.SWo), v[r]);
-      } else {
-#pragma unroll
-        for (int r = 0; r < R; r++) {
-          const int k = k0 + pp.L * r;
-          emit_fold<T, M, RATIO>(v[r], r, k, n, coef, acc, dump);
-        }
       }
       __syncthreads();
     }
@@ -746,12 +781,14 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
     cert_flush(acc, cs);
     __syncthreads();
     if (LAST16) {  // restore the forward-last table for the next pair of this CTA
-      if (threadIdx.x == 0 && pair + (int)gridDim.x < kp.batch)
-        bulk_load(twb, tw + Gm::tw_fwd(Gm::P.nf - 1), FL_BYTES, &tbar);
+      if (threadIdx.x == 0 && nxt < kp.batch) {
+        mbar_expect(&tbar, FL_BYTES);
+        bulk_copy(twb, tw + Gm::tw_fwd(Gm::P.nf - 1), FL_BYTES, &tbar);
+      }
       pending = true;
     }
     const bool certified = cs.ok != 0;
-    carry_store(coef, n, kp.prod + (size_t)pair * 2 * n, certified, reinterpret_cast<uint16_t *>(smem));
+    carry_store(coef, n, kp.prod + (size_t)pair * 2 * n, certified, ubuf);
     if (kp.coeffs) {
       int64_t *co = kp.coeffs + (size_t)pair * (2 * n - 1);
       for (int i = threadIdx.x; i < 2 * n - 1; i += blockDim.x) co[i] = certified ? coef[i] : 0;
