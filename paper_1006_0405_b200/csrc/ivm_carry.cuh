@@ -1,67 +1,144 @@
 // ivm_carry.cuh -- carry of snapped coefficients to base-256 digits.
 //
-// c_i < 2^31 is split into bytes: t_i = sum_b byte_b(c_{i-b}) <= 1020,
-// u_i = (t_i & 255) + (t_{i-1} >> 8) <= 258, so sum_i c_i 256^i = sum_i u_i 256^i
-// and every remaining carry is 0 or 1: generate g_i = (u_i >= 256), propagate
-// p_i = (u_i == 255); carries by a carry-lookahead over warp ballots
-// (cin = ((G | P) + G + c0) ^ P), a block scan over warps, then one pass.
+// Word form of the carry.  Four digit positions make one 32-bit word:
+//   V_k = sum_{b<4} c_{4k+b} 256^b  (< 2^56 for 0 <= c_i < 2^31),  sum_i c_i 256^i = sum_k V_k 2^{32k}.
+// With V_k = lo_k + hi_k 2^32 the word sums W_k = lo_k + hi_{k-1} < 2^33 and
+// u_k = (W_k mod 2^32) + floor(W_{k-1} / 2^32) <= 2^32 leave carries of 0 or 1:
+// generate g_k = (u_k == 2^32), propagate p_k = (u_k == 2^32 - 1), and the
+// carry into word k is c_k = g_{k-1} | (p_{k-1} & c_{k-1}).  Inside a warp the
+// 32 carries of one step come from the ballot adder cin = ((G|P) + G + c0) ^ P
+// (bit l of the sum (G|P) + G + c0 is the carry into lane l, complemented where
+// P_l), across warps from one more ballot scan; the digits are the bytes of
+// (u_k + c_k) mod 2^32.  Lane l of warp w handles word k = w SEG + 32 j + l, so
+// the coefficient reads (16 B per lane) and the digit stores are contiguous.
 #pragma once
 #include <stdint.h>
 
 namespace ivm {
 
-// coef: [2n-1] int32 (shared); ubuf: >= 2n+4 uint16 scratch (shared)
-static __device__ __forceinline__ void carry_store(const int32_t *coef, int n, uint8_t *__restrict__ out, bool certified,
-                                   uint16_t *ubuf) {
-  const int nout = 2 * n;
+// word k of the split: (low 32 bits, high bits) of V_k; c_i = 0 outside [0, nc)
+static __device__ __forceinline__ void carry_word(const int32_t *coef, int nc, int k, unsigned &lo,
+                                                  unsigned &hi) {
+  if (k < 0 || 4 * k >= nc) {
+    lo = hi = 0u;
+    return;
+  }
+  unsigned c0, c1, c2, c3;
+  if (4 * k + 3 < nc) {
+    const int4 q = reinterpret_cast<const int4 *>(coef)[k];
+    c0 = (unsigned)q.x, c1 = (unsigned)q.y, c2 = (unsigned)q.z, c3 = (unsigned)q.w;
+  } else {
+    c0 = (unsigned)coef[4 * k];
+    c1 = 4 * k + 1 < nc ? (unsigned)coef[4 * k + 1] : 0u;
+    c2 = 4 * k + 2 < nc ? (unsigned)coef[4 * k + 2] : 0u;
+    c3 = 0u;
+  }
+  const unsigned long long v = (unsigned long long)c0 + ((unsigned long long)c1 << 8) +
+                               ((unsigned long long)c2 << 16) + ((unsigned long long)c3 << 24);
+  lo = (unsigned)v;
+  hi = (unsigned)(v >> 32);
+}
+
+// per step: u (mod 2^32) and the generate / propagate bits of this lane's word.
+// hprev / eprev: hi_{k-1} and floor(W_{k-1} / 2^32) of the word below lane 0.
+struct CarryStep {
+  unsigned u;
+  bool g, p;
+  unsigned hi_top, ov_top;  // lane 31's hi and overflow, for the next step's lane 0
+};
+static __device__ __forceinline__ CarryStep carry_step(const int32_t *coef, int nc, int k, unsigned lane,
+                                                       unsigned hprev, unsigned eprev) {
+  unsigned lo, hi;
+  carry_word(coef, nc, k, lo, hi);
+  unsigned hp = __shfl_up_sync(0xffffffffu, hi, 1);
+  if (lane == 0) hp = hprev;
+  const unsigned w = lo + hp;
+  const unsigned ov = w < lo ? 1u : 0u;  // floor(W_k / 2^32)
+  unsigned ep = __shfl_up_sync(0xffffffffu, ov, 1);
+  if (lane == 0) ep = eprev;
+  CarryStep s;
+  s.u = w + ep;
+  s.g = ep != 0u && w == 0xffffffffu;
+  s.p = s.u == 0xffffffffu && !s.g;
+  s.hi_top = __shfl_sync(0xffffffffu, hi, 31);
+  s.ov_top = __shfl_sync(0xffffffffu, ov, 31);
+  return s;
+}
+
+// coef: [2n-1] int32, 16-byte aligned (shared); out: [2n] digits (global).
+// Every thread of the block calls it (blockDim.x a multiple of 32, <= 1024).
+static __device__ __forceinline__ void carry_store(const int32_t *coef, int n, uint8_t *__restrict__ out,
+                                                   bool certified) {
+  const int nout = 2 * n, nc = 2 * n - 1;
   if (!certified) {
     for (int i = threadIdx.x; i < nout; i += blockDim.x) out[i] = 0;
     return;
   }
-  const int nc = 2 * n - 1, npos = 2 * n + 4;
-  const int T = blockDim.x, K = (npos + T - 1) / T;
-  const int p0 = threadIdx.x * K, p1 = min(p0 + K, npos);
-  // sliding window: c_{i-3..i}, t_{i-1}
-  auto cget = [&](int i) -> unsigned { return (i >= 0 && i < nc) ? (unsigned)coef[i] : 0u; };
-  unsigned c1 = cget(p0 - 1), c2 = cget(p0 - 2), c3 = cget(p0 - 3), c4 = cget(p0 - 4);
-  int tprev = (int)((c1 & 255) + ((c2 >> 8) & 255) + ((c3 >> 16) & 255) + (c4 >> 24));
-  int c = 0;
-  bool allp = true;
-  for (int i = p0; i < p1; i++) {
-    const unsigned c0 = cget(i);
-    const int t = (int)((c0 & 255) + ((c1 >> 8) & 255) + ((c2 >> 16) & 255) + (c3 >> 24));
-    const int u = (t & 255) + (tprev >> 8);
-    ubuf[i] = (uint16_t)u;
-    allp = allp && (u == 255);
-    c = (u + c) >> 8;
-    tprev = t;
-    c3 = c2;
-    c2 = c1;
-    c1 = c0;
+  const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int words = (nout + 3) / 4;
+  const int J = (words + 32 * (int)nwarps - 1) / (32 * (int)nwarps);  // steps per warp
+  const int k0 = (int)warp * 32 * J;
+  // the two words below the segment: hi_{k0-1}, floor(W_{k0-1} / 2^32)
+  unsigned hprev, eprev;
+  {
+    unsigned l1, h1, l2, h2;
+    carry_word(coef, nc, k0 - 1, l1, h1);
+    carry_word(coef, nc, k0 - 2, l2, h2);
+    hprev = h1;
+    eprev = (l1 + h2) < l1 ? 1u : 0u;
   }
-  const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = (T + 31) >> 5;
-  const unsigned g = __ballot_sync(0xffffffffu, c != 0), p = __ballot_sync(0xffffffffu, allp);
+  // pass 1: the segment's generate (carry out with carry in 0) and all-propagate
+  unsigned c = 0u;
+  bool allp = true;
+  {
+    unsigned hp = hprev, ep = eprev;
+    for (int j = 0; j < J; j++) {
+      const int k = k0 + 32 * j + (int)lane;
+      const CarryStep s = carry_step(coef, nc, k, lane, hp, ep);
+      const unsigned G = __ballot_sync(0xffffffffu, s.g), P = __ballot_sync(0xffffffffu, s.p);
+      const unsigned long long S = (unsigned long long)(G | P) + G + c;
+      c = (unsigned)(S >> 32);
+      allp = allp && (P == 0xffffffffu);
+      hp = s.hi_top;
+      ep = s.ov_top;
+    }
+  }
   __shared__ unsigned wg[32], wp[32], wc[32];
   if (lane == 0) {
-    const unsigned long long s = (unsigned long long)(g | p) + g;
-    wg[warp] = (unsigned)(s >> 32);
-    wp[warp] = (p == 0xffffffffu);
+    wg[warp] = c;
+    wp[warp] = allp ? 1u : 0u;
   }
   __syncthreads();
   if (warp == 0) {
     const bool gg = lane < nwarps ? wg[lane] != 0 : false;
-    const bool pp = lane < nwarps ? wp[lane] != 0 : true;
+    const bool pp = lane < nwarps ? wp[lane] != 0 : false;
     const unsigned G2 = __ballot_sync(0xffffffffu, gg), P2 = __ballot_sync(0xffffffffu, pp);
     const unsigned cin = ((G2 | P2) + G2) ^ P2;
     if (lane < nwarps) wc[lane] = (cin >> lane) & 1u;
   }
   __syncthreads();
-  const unsigned long long s = (unsigned long long)(g | p) + g + wc[warp];
-  int cc = (int)((((unsigned)s ^ p) >> lane) & 1u);
-  for (int i = p0; i < p1; i++) {
-    const int u = (int)ubuf[i] + cc;
-    if (i < nout) out[i] = (uint8_t)(u & 255);
-    cc = u >> 8;
+  // pass 2: carries into every word, digits out
+  c = wc[warp];
+  const bool wide = (reinterpret_cast<uintptr_t>(out) & 3) == 0;
+  unsigned hp = hprev, ep = eprev;
+  for (int j = 0; j < J; j++) {
+    const int k = k0 + 32 * j + (int)lane;
+    const CarryStep s = carry_step(coef, nc, k, lane, hp, ep);
+    const unsigned G = __ballot_sync(0xffffffffu, s.g), P = __ballot_sync(0xffffffffu, s.p);
+    const unsigned long long S = (unsigned long long)(G | P) + G + c;
+    const unsigned cl = (((unsigned)S ^ P) >> lane) & 1u;
+    c = (unsigned)(S >> 32);
+    hp = s.hi_top;
+    ep = s.ov_top;
+    const unsigned d = s.u + cl;
+    const int i = 4 * k;
+    if (i + 3 < nout && wide) {
+      *reinterpret_cast<unsigned *>(out + i) = d;
+    } else {
+#pragma unroll
+      for (int b = 0; b < 4; b++)
+        if (i + b < nout) out[i + b] = (uint8_t)(d >> (8 * b));
+    }
   }
 }
 

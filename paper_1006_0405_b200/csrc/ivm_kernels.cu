@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(Cfg<T, M>::THREADS, 1) ivm_cta_kernel(KParams 
     inv_last<T, N, QlastI, LlastI>(st, tw, n, coef, cs, dump);
     __syncthreads();
     const bool certified = cs.ok != 0;
-    carry_store(coef, n, kp.prod + (size_t)pair * 2 * n, certified, reinterpret_cast<uint16_t *>(smem));
+    carry_store(coef, n, kp.prod + (size_t)pair * 2 * n, certified);
     if (kp.coeffs) {
       int64_t *co = kp.coeffs + (size_t)pair * (2 * n - 1);
       for (int i = threadIdx.x; i < 2 * n - 1; i += blockDim.x) co[i] = coef[i];

@@ -612,8 +612,8 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phas
 }
 
 // shared memory of the one-CTA kernel (bytes):
-//   [state: 2 planes x CAP]  (the int32 coefficients and the carry scratch alias
-//                             it once the last inverse pass has loaded its inputs)
+//   [state: 2 planes x CAP]  (the int32 coefficients alias it once the last
+//                             inverse pass has loaded its inputs)
 //   [twiddles: big buffer (forward-last table <-> folded inverse table) + the
 //              resident mid-pass tables]
 //   [digits: a | b of the current pair, staged by a bulk copy one pair ahead]
@@ -625,12 +625,11 @@ template <typename T, int M, int R> struct Cfg3 {
   static constexpr size_t E = sizeof(typename V2t<T>::t);
   static constexpr size_t STATE_BYTES = 2 * E * (size_t)CAP;
   static constexpr size_t COEF_BYTES = 4 * (size_t)N;
-  static constexpr size_t UBUF_BYTES = 2 * ((size_t)N + 8);
   static constexpr size_t A_BYTES = 2 * E * (size_t)(N / 2);  // [R][L/2] x (re, im)
   static constexpr size_t TW_BYTES = sizeof(TwC<T>) * (size_t)Gm::SM_ENT();
   static constexpr size_t DIG_BYTES = (size_t)N;  // 2n <= N
   static constexpr size_t SMEM = STATE_BYTES + TW_BYTES + DIG_BYTES;
-  static_assert(STATE_BYTES >= COEF_BYTES + UBUF_BYTES, "coefficients + carry scratch alias the state");
+  static_assert(STATE_BYTES >= COEF_BYTES, "the coefficients alias the state");
   static_assert(SMEM <= 227 * 1024, "shared memory");
 };
 
@@ -645,7 +644,6 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
   __shared__ __align__(8) unsigned long long tbar, dbar;
   Buf<T> st{reinterpret_cast<V *>(smem), reinterpret_cast<V *>(smem) + C::CAP};
   int32_t *coef = reinterpret_cast<int32_t *>(smem);  // aliases the state (see Cfg3)
-  uint16_t *ubuf = reinterpret_cast<uint16_t *>(smem + C::COEF_BYTES);
   TwC<T> *twb = reinterpret_cast<TwC<T> *>(smem + C::STATE_BYTES);
   uint8_t *sdig = smem + C::STATE_BYTES + C::TW_BYTES;
   Buf<T> A{reinterpret_cast<V *>(kp.ascratch) + (size_t)blockIdx.x * N, nullptr};
@@ -788,7 +786,7 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
       pending = true;
     }
     const bool certified = cs.ok != 0;
-    carry_store(coef, n, kp.prod + (size_t)pair * 2 * n, certified, ubuf);
+    carry_store(coef, n, kp.prod + (size_t)pair * 2 * n, certified);
     if (kp.coeffs) {
       int64_t *co = kp.coeffs + (size_t)pair * (2 * n - 1);
       for (int i = threadIdx.x; i < 2 * n - 1; i += blockDim.x) co[i] = certified ? coef[i] : 0;
