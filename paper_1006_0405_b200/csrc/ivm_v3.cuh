@@ -677,8 +677,12 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
       bulk_copy(sdig + n, kp.b + (size_t)blockIdx.x * n, n, &dbar);
     }
   }
-  unsigned ph = 0, dph = 0;
-  bool pending = true;
+  // tbar phases: 0 = initial tables; per pair (LAST16) the folded table and
+  // then the forward-last restore, so the folded-table wait has parity 1 and the
+  // forward-last wait parity 0 (trivially complete in the first pair).  dbar:
+  // one phase per pair.
+  if (blockIdx.x < kp.batch) mbar_wait(&tbar, 0);
+  unsigned dph = 0;
 
   for (int pair = blockIdx.x; pair < kp.batch; pair += gridDim.x) {
     const int nxt = pair + (int)gridDim.x;
@@ -717,11 +721,7 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
         const PassRT pp = pick_fwd<M, R>(i);
         CI<T> v[R];
         int k0, nu;
-        if (pp.big && pending) {
-          mbar_wait(&tbar, ph);
-          ph ^= 1u;
-          pending = false;
-        }
+        if (LAST16 && op == 0 && pp.big) mbar_wait(&tbar, 0);  // forward-last table restored
         fwdR<T, R>(st, twb, pp, v, k0, nu);
         if (i < NFWD - 1) {  // mid pass: store both halves (mirror conjugated)
           __syncthreads();
@@ -734,20 +734,24 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
 #pragma unroll
           for (int r = 0; r < R; r++) A.st(r * (pp.L >> 1) + k0, v[r]);
         } else {  // last pass of b + pointwise + inverse pass 0
+          // A from L2, one load in flight ahead of the product
+          CI<T> an = A.ld(k0);
 #pragma unroll
-          for (int r = 0; r < R; r++) v[r] = cmul(A.ld(r * (pp.L >> 1) + k0), v[r]);
+          for (int r = 0; r < R; r++) {
+            const CI<T> a = an;
+            if (r + 1 < R) an = A.ld((r + 1) * (pp.L >> 1) + k0);
+            v[r] = cmul(a, v[r]);
+          }
           cdft<T, R, true>(v);
           __syncthreads();
 #pragma unroll
           for (int r = 0; r < R; r++) st.st(sidx(r, k0, RSI1, SWI1), v[r]);
         }
         __syncthreads();
-        if (LAST16 && op == 1 && i == NFWD - 1) {
-          if (threadIdx.x == 0) {  // the folded inverse table replaces the forward-last one
-            mbar_expect(&tbar, L16_BYTES);
-            bulk_copy(twb, tw + Gm::tw_l16(), L16_BYTES, &tbar);
-          }
-          pending = true;
+        if (LAST16 && op == 1 && i == NFWD - 1 && threadIdx.x == 0) {
+          // the folded inverse table replaces the forward-last one
+          mbar_expect(&tbar, L16_BYTES);
+          bulk_copy(twb, tw + Gm::tw_l16(), L16_BYTES, &tbar);
         }
       }
     }
@@ -757,12 +761,8 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
       const PassRT pp = pick_inv<M, R>(i);
       CI<T> v[R];
       int k0, nu;
-      if (pp.big && pending) {
-        mbar_wait(&tbar, ph);
-        ph ^= 1u;
-        pending = false;
-      }
       if (LAST16 && i == NINV - 1) {
+        mbar_wait(&tbar, 1);  // folded table
         invR<T, R, true>(st, twb, pp, v, k0, nu);
         __syncthreads();  // every input loaded: the coefficients may overwrite the state
 #pragma unroll
@@ -778,12 +778,9 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
     if constexpr (!LAST16) inv_last<T, M, R>(st, tw, n, coef, acc, dump);
     cert_flush(acc, cs);
     __syncthreads();
-    if (LAST16) {  // restore the forward-last table for the next pair of this CTA
-      if (threadIdx.x == 0 && nxt < kp.batch) {
-        mbar_expect(&tbar, FL_BYTES);
-        bulk_copy(twb, tw + Gm::tw_fwd(Gm::P.nf - 1), FL_BYTES, &tbar);
-      }
-      pending = true;
+    if (LAST16 && threadIdx.x == 0 && nxt < kp.batch) {  // restore the forward-last table
+      mbar_expect(&tbar, FL_BYTES);
+      bulk_copy(twb, tw + Gm::tw_fwd(Gm::P.nf - 1), FL_BYTES, &tbar);
     }
     const bool certified = cs.ok != 0;
     carry_store(coef, n, kp.prod + (size_t)pair * 2 * n, certified);
