@@ -633,6 +633,13 @@ template <typename T, int M, int R> struct Cfg3 {
   static_assert(SMEM <= 227 * 1024, "shared memory");
 };
 
+// diagnostic interval dump of this pair (ivm_multiply_batched_diag), else null
+__device__ __forceinline__ double *diag_dump(const KParams &kp, int pair, int N) {
+  if (!kp.dump_slot) return nullptr;
+  const int s = kp.dump_slot[pair];
+  return s >= 0 ? kp.intervals + (size_t)s * N * 4 : nullptr;
+}
+
 template <typename T, int M, int R>
 __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) ivm_v3_kernel(KParams kp) {
   using C = Cfg3<T, M, R>;
@@ -682,8 +689,6 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
   // forward-last wait parity 0 (trivially complete in the first pair).  dbar:
   // one phase per pair.
   if (blockIdx.x < kp.batch) mbar_wait(&tbar, 0);
-  unsigned dph = 0;
-
   for (int pair = blockIdx.x; pair < kp.batch; pair += gridDim.x) {
     const int nxt = pair + (int)gridDim.x;
     if (!staged && nxt < kp.batch) {  // L2 prefetch of the next pair's digits
@@ -692,15 +697,7 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
         asm volatile("prefetch.global.L2 [%0];" ::"l"(kp.b + (size_t)nxt * n + off));
       }
     }
-    if (staged) {
-      mbar_wait(&dbar, dph);
-      dph ^= 1u;
-    }
-    double *dump = nullptr;
-    if (kp.dump_slot) {
-      const int s = kp.dump_slot[pair];
-      if (s >= 0) dump = kp.intervals + (size_t)s * N * 4;
-    }
+    if (staged) mbar_wait(&dbar, (unsigned)((pair - (int)blockIdx.x) / (int)gridDim.x) & 1u);
 #pragma unroll 1
     for (int op = 0; op < 2; op++) {
       const uint8_t *dig = staged ? sdig + op * n : (op == 0 ? kp.a : kp.b) + (size_t)pair * n;
@@ -744,15 +741,14 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
           }
           cdft<T, R, true>(v);
           __syncthreads();
+          if (LAST16 && threadIdx.x == 0) {  // the folded inverse table replaces the forward-last one
+            mbar_expect(&tbar, L16_BYTES);
+            bulk_copy(twb, tw + Gm::tw_l16(), L16_BYTES, &tbar);
+          }
 #pragma unroll
           for (int r = 0; r < R; r++) st.st(sidx(r, k0, RSI1, SWI1), v[r]);
         }
         __syncthreads();
-        if (LAST16 && op == 1 && i == NFWD - 1 && threadIdx.x == 0) {
-          // the folded inverse table replaces the forward-last one
-          mbar_expect(&tbar, L16_BYTES);
-          bulk_copy(twb, tw + Gm::tw_l16(), L16_BYTES, &tbar);
-        }
       }
     }
     CertAcc acc;
@@ -765,6 +761,7 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
         mbar_wait(&tbar, 1);  // folded table
         invR<T, R, true>(st, twb, pp, v, k0, nu);
         __syncthreads();  // every input loaded: the coefficients may overwrite the state
+        double *dump = diag_dump(kp, pair, N);
 #pragma unroll
         for (int r = 0; r < R; r++) emit_fold<T, M, RATIO>(v[r], r, k0 + pp.L * r, n, coef, acc, dump);
       } else {
@@ -775,7 +772,7 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
       }
       __syncthreads();
     }
-    if constexpr (!LAST16) inv_last<T, M, R>(st, tw, n, coef, acc, dump);
+    if constexpr (!LAST16) inv_last<T, M, R>(st, tw, n, coef, acc, diag_dump(kp, pair, N));
     cert_flush(acc, cs);
     __syncthreads();
     if (LAST16 && threadIdx.x == 0 && nxt < kp.batch) {  // restore the forward-last table
