@@ -112,8 +112,13 @@ int ivm_multiply_batched_diag(ivm_ctx_t ctx, const uint8_t *a, const uint8_t *b,
 
 /* Host-pointer convenience (end-to-end path): copies a, b (host, [batch][n])
  * to the device, multiplies, and copies prod / certified back to host
- * buffers, all on `cuda_stream`; returns after the stream is synchronised.
- * Uses context-owned device staging buffers. */
+ * buffers; returns after `cuda_stream` is synchronised.  The batch is cut into
+ * at most 8 chunks of whole waves (multiples of the SM count): chunk i's
+ * kernel runs on `cuda_stream` while chunk i+1 is copied in and chunk i-1
+ * copied out on two context-owned streams (event-ordered; work queued on
+ * `cuda_stream` before the call is waited for).  Host buffers should be
+ * pinned for the copies to overlap.  Uses context-owned device staging
+ * buffers (2 n batch + 2 n batch + batch bytes). */
 int ivm_multiply_batched_host(ivm_ctx_t ctx, const uint8_t *a, const uint8_t *b, size_t n,
                               size_t batch, uint8_t *prod, uint8_t *certified, int prec,
                               void *cuda_stream);

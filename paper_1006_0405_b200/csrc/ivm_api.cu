@@ -35,6 +35,9 @@ struct ivm_ctx {
   int last_launches = 0;
   void *gscratch = nullptr;  // large-m group scratch
   size_t gscratch_bytes = 0;
+  // host API pipeline: copy-in / copy-out streams and per-chunk events
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  std::vector<cudaEvent_t> ev;
 };
 
 static int cuda_fail(ivm_ctx_t c) {
@@ -128,6 +131,9 @@ int ivm_destroy(ivm_ctx_t c) {
   cudaFree(c->slot);
   cudaFree(c->stage);
   cudaFree(c->gscratch);
+  if (c->s_in) cudaStreamDestroy(c->s_in);
+  if (c->s_out) cudaStreamDestroy(c->s_out);
+  for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   delete c;
   return IVM_OK;
 }
@@ -382,14 +388,53 @@ int ivm_multiply_batched_host(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, s
     if (cudaMalloc(&c->stage, need) != cudaSuccess) return IVM_ENOMEM;
     c->stage_bytes = need;
   }
+  if (!c->s_in) {
+    if (cudaStreamCreateWithFlags(&c->s_in, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking) != cudaSuccess)
+      return cuda_fail(c);
+  }
+  // chunks of whole waves (multiples of the SM count), at most kChunks: the
+  // copy-in of chunk i+1 and the copy-out of chunk i-1 overlap the kernel of chunk i
+  const int kChunks = 8;
+  const size_t sms = (size_t)(c->sms > 0 ? c->sms : 1);
+  size_t chunk = batch;
+  if (batch >= 2 * sms) {
+    chunk = (batch + kChunks - 1) / kChunks;
+    chunk = (chunk + sms - 1) / sms * sms;
+  }
+  const size_t nchunks = (batch + chunk - 1) / chunk;
+  while (c->ev.size() < 3 * nchunks + 1) {
+    cudaEvent_t e;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return cuda_fail(c);
+    c->ev.push_back(e);
+  }
   cudaStream_t s = (cudaStream_t)stream;
   uint8_t *da = c->stage, *db = da + in, *dp = db + in, *dc = dp + out;
-  if (cudaMemcpyAsync(da, a, in, cudaMemcpyHostToDevice, s) != cudaSuccess) return cuda_fail(c);
-  if (cudaMemcpyAsync(db, b, in, cudaMemcpyHostToDevice, s) != cudaSuccess) return cuda_fail(c);
-  r = ivm_multiply_batched(c, da, db, n, batch, dp, dc, prec, stream);
-  if (r) return r;
-  if (cudaMemcpyAsync(prod, dp, out, cudaMemcpyDeviceToHost, s) != cudaSuccess) return cuda_fail(c);
-  if (cudaMemcpyAsync(cert, dc, batch, cudaMemcpyDeviceToHost, s) != cudaSuccess) return cuda_fail(c);
+  // the internal streams start after the work already queued on `stream`
+  cudaEvent_t e0 = c->ev[3 * nchunks];
+  if (cudaEventRecord(e0, s) != cudaSuccess || cudaStreamWaitEvent(c->s_in, e0, 0) != cudaSuccess)
+    return cuda_fail(c);
+  int launches = 0;
+  for (size_t k = 0; k < nchunks; k++) {
+    const size_t p0 = k * chunk, bk = (batch - p0 < chunk) ? batch - p0 : chunk;
+    cudaEvent_t e_in = c->ev[3 * k], e_run = c->ev[3 * k + 1], e_out = c->ev[3 * k + 2];
+    if (cudaMemcpyAsync(da + p0 * n, a + p0 * n, bk * n, cudaMemcpyHostToDevice, c->s_in) != cudaSuccess ||
+        cudaMemcpyAsync(db + p0 * n, b + p0 * n, bk * n, cudaMemcpyHostToDevice, c->s_in) != cudaSuccess ||
+        cudaEventRecord(e_in, c->s_in) != cudaSuccess || cudaStreamWaitEvent(s, e_in, 0) != cudaSuccess)
+      return cuda_fail(c);
+    r = ivm_multiply_batched(c, da + p0 * n, db + p0 * n, n, bk, dp + p0 * 2 * n, dc + p0, prec, stream);
+    if (r) return r;
+    launches += c->last_launches;
+    if (cudaEventRecord(e_run, s) != cudaSuccess || cudaStreamWaitEvent(c->s_out, e_run, 0) != cudaSuccess ||
+        cudaMemcpyAsync(prod + p0 * 2 * n, dp + p0 * 2 * n, bk * 2 * n, cudaMemcpyDeviceToHost, c->s_out) !=
+            cudaSuccess ||
+        cudaMemcpyAsync(cert + p0, dc + p0, bk, cudaMemcpyDeviceToHost, c->s_out) != cudaSuccess ||
+        cudaEventRecord(e_out, c->s_out) != cudaSuccess)
+      return cuda_fail(c);
+  }
+  // `stream` completes after the last copy-out
+  if (cudaStreamWaitEvent(s, c->ev[3 * (nchunks - 1) + 2], 0) != cudaSuccess) return cuda_fail(c);
+  c->last_launches = launches;
   if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_fail(c);
   return IVM_OK;
 }

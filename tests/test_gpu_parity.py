@@ -179,6 +179,26 @@ def test_host_entry_point_matches_device(ctx):
     assert np.array_equal(out.numpy(), oracle.long_multiply(a, b))
 
 
+@pytest.mark.parametrize("n,batch", [(200, 1000), (2048, 700), (1000, 2 * 148 + 3)])
+def test_host_entry_point_chunked_pipeline(ctx, n, batch):
+    """Batches of >= 2 waves go through the chunked copy/compute pipeline: the
+    result must equal the device-pointer path pair by pair, with the unequal
+    last chunk included; a sample of pairs is checked against the oracle."""
+    import torch
+    K = inputs.KINDS
+    kinds = np.array([K["uniform"], K["all255"], K["sparse"]])[np.arange(batch) % 3]
+    a, b = inputs.pair_digits(13, np.arange(batch), n, kinds)
+    pa = torch.from_numpy(a).pin_memory()
+    pb = torch.from_numpy(b).pin_memory()
+    out, cert = ctx.multiply_host(pa, pb)
+    dout, dcert = ctx.multiply(pa.cuda(), pb.cuda())
+    assert np.array_equal(out.numpy(), dout.cpu().numpy())
+    assert np.array_equal(cert.numpy(), dcert.cpu().numpy())
+    assert cert.numpy().all()
+    idx = np.array([0, batch // 2, batch - 1])
+    assert np.array_equal(out.numpy()[idx], oracle.long_multiply(a[idx], b[idx]))
+
+
 def test_argument_errors(ctx):
     import torch
     import paper_1006_0405_b200 as ivm
