@@ -50,6 +50,22 @@ def W_ops(m: int) -> int:
     return 24 * m * L - 28 * m + 48
 
 
+def load_traffic(config: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    --set full capture of this config (latest round under profiles/), else None."""
+    try:
+        rounds = sorted(d for d in os.listdir(os.path.join(ROOT, "profiles")) if d.startswith("r"))
+        for r in reversed(rounds):
+            f = os.path.join(ROOT, "profiles", r, "ncu_traffic.json")
+            if os.path.exists(f):
+                t = json.load(open(f)).get(config)
+                if t:
+                    return t["dram_bytes_per_launch"]
+    except Exception:
+        pass
+    return None
+
+
 def load_peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -317,7 +333,8 @@ def run_ours(args):
                        "gather_to_rank0_ms": gather_ms},
             "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12,
                          "unit": "Top/s (directed FP64 DADD/DMUL/DFMA, FMA = 1 op)",
-                         "frac": achieved / peak_ops, "traffic": None,
+                         "frac": achieved / peak_ops, "traffic": load_traffic(args.config),
+                         "traffic_unit": "DRAM bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
                          "work_per_unit": f"W(m) = 24 m log2 m - 28 m + 48 = {W_ops(m)} ops per multiplication (SURVEY.md 8(d.1))",
                          "peak_basis": f"148 SM x 64 FP64 lanes x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz); directed-DFMA probe measured {probe/1e12 if probe else float('nan'):.2f} Top/s",
                          "kernel_ms": ms_per_step},
