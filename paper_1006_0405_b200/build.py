@@ -22,7 +22,7 @@ NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--ft
                   "-I", os.path.join(ROOT, "include")]
 CXXFLAGS = ["-O2", "-fPIC", "-std=gnu++17", "-fext-numeric-literals", "-I", os.path.join(ROOT, "include")]
 
-CU = ["ivm_kernels.cu", "ivm_v3.cu", "ivm_api.cu"]
+CU = ["ivm_kernels.cu", "ivm_v3.cu", "ivm_v4.cu", "ivm_api.cu"]
 CPP = ["ivm_planner.cpp"]
 HDR = ["ivm_interval.cuh", "ivm_fft.cuh", "ivm_internal.h", "ivm_carry.cuh", "ivm_v3.cuh"]
 

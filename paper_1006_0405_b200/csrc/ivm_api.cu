@@ -25,6 +25,9 @@ struct ivm_ctx {
   std::map<std::pair<int, int>, ivm::LaunchInfo> info;
   std::map<std::pair<int, int>, ivm::LaunchInfo> info3;
   bool force_v1 = false;
+  bool force_v3g = false;  // IVM_KERNEL=v3g: the global-memory group kernel for m = 2^14 .. 2^16 too
+  std::map<std::pair<int, int>, void *> tw4;  // (log2m, prec) -> v4 role tables
+  std::map<std::pair<int, int>, ivm::LaunchInfo> info4;
   int radix = 8;  // radix of the one-CTA kernel
   void *ascratch = nullptr;
   size_t ascratch_bytes = 0;
@@ -110,13 +113,14 @@ int ivm_create(ivm_ctx_t *ctx, int device) {
       delete c;
       return IVM_EUNSUPPORTED;
     }
-    if (ivm::upload_w64(t64, t32) != 0) {
+    if (ivm::upload_w64(t64, t32) != 0 || ivm::upload_w64_v4(t64, t32) != 0) {
       delete c;
       return IVM_ECUDA;
     }
   }
   const char *kv = getenv("IVM_KERNEL");
   c->force_v1 = kv && strcmp(kv, "v1") == 0;
+  c->force_v3g = kv && strcmp(kv, "v3g") == 0;
   c->consts = true;
   *ctx = c;
   return IVM_OK;
@@ -127,6 +131,7 @@ int ivm_destroy(ivm_ctx_t c) {
   cudaSetDevice(c->device);
   for (auto &kv : c->tw) cudaFree(kv.second);
   for (auto &kv : c->tw3) cudaFree(kv.second);
+  for (auto &kv : c->tw4) cudaFree(kv.second);
   cudaFree(c->ascratch);
   cudaFree(c->slot);
   cudaFree(c->stage);
@@ -160,7 +165,47 @@ static int get_table(ivm_ctx_t c, int m, int prec, const void **out) {
 }
 
 static bool use_v3(ivm_ctx_t c, int m) { return !c->force_v1 && m >= 10 && m <= 13; }
-static bool use_v3g(int m) { return m >= 14 && m <= 18; }
+static bool use_v4(ivm_ctx_t c, int m) { return !c->force_v3g && m >= 14 && m <= 16; }
+static bool use_v3g(ivm_ctx_t c, int m) { return m >= 14 && m <= 18 && !use_v4(c, m); }
+
+static int get_table4(ivm_ctx_t c, int m, int prec, const void **out) {
+  auto key = std::make_pair(m, prec);
+  auto it = c->tw4.find(key);
+  if (it != c->tw4.end()) {
+    *out = it->second;
+    return IVM_OK;
+  }
+  const size_t N2 = (size_t)2 << m, es = prec == IVM_F64 ? 8 : 4;
+  std::vector<unsigned char> w2N(N2 * 4 * es);
+  if (ivm::plan_twiddles(m + 1, prec, w2N.data()) != 0) return IVM_EUNSUPPORTED;
+  const int ent = ivm::v4_table_entries(m);
+  if (ent < 0) return IVM_EUNSUPPORTED;
+  std::vector<unsigned char> h((size_t)ent * 2 * es);
+  if (ivm::v4_tables(m, prec, w2N.data(), h.data()) != ent) return IVM_EUNSUPPORTED;
+  void *d = nullptr;
+  if (cudaMalloc(&d, h.size()) != cudaSuccess) return IVM_ENOMEM;
+  if (cudaMemcpy(d, h.data(), h.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(d);
+    return cuda_fail(c);
+  }
+  c->tw4[key] = d;
+  *out = d;
+  return IVM_OK;
+}
+
+static int get_info4(ivm_ctx_t c, int m, int prec, ivm::LaunchInfo *li) {
+  auto key = std::make_pair(m, prec);
+  auto it = c->info4.find(key);
+  if (it != c->info4.end()) {
+    *li = it->second;
+    return IVM_OK;
+  }
+  int r = ivm::v4_info(prec, m, li);
+  if (r == -4) return IVM_EUNSUPPORTED;
+  if (r != 0 || li->max_clusters < 1) return cuda_fail(c);
+  c->info4[key] = *li;
+  return IVM_OK;
+}
 
 static int get_table3(ivm_ctx_t c, int m, int prec, const void **out) {
   const int radix = (m >= 10 && m <= 13) ? c->radix : 16;
@@ -248,7 +293,16 @@ int ivm_reserve(ivm_ctx_t c, size_t n, size_t batch, int prec) {
   if (cudaSetDevice(c->device) != cudaSuccess) return cuda_fail(c);
   int m = log2m_for(n);
   if (m < 2) return IVM_OK;
-  if (use_v3g(m)) {
+  if (use_v4(c, m)) {
+    const void *t4;
+    ivm::LaunchInfo li;
+    int r = get_table4(c, m, prec, &t4);
+    if (!r) r = get_info4(c, m, prec, &li);
+    if (r) return r;
+    size_t cl = (size_t)li.max_clusters < batch ? (size_t)li.max_clusters : batch;
+    return ensure_scratch(c, cl * li.cluster * li.a_bytes_per_cta);
+  }
+  if (use_v3g(c, m)) {
     const void *t3;
     return get_table3(c, m, prec, &t3);
   }
@@ -302,7 +356,22 @@ int ivm_multiply_batched_diag(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, s
     c->last_launches = launches + 1;
     return IVM_OK;
   }
-  if (use_v3g(m)) {
+  if (use_v4(c, m)) {
+    const void *tw;
+    ivm::LaunchInfo li;
+    r = get_table4(c, m, prec, &tw);
+    if (!r) r = get_info4(c, m, prec, &li);
+    if (r) return r;
+    const size_t cl = (size_t)li.max_clusters < batch ? (size_t)li.max_clusters : batch;
+    r = ensure_scratch(c, cl * li.cluster * li.a_bytes_per_cta);
+    if (r) return r;
+    kp.ascratch = c->ascratch;
+    kp.tw = tw;
+    if (ivm::v4_launch(prec, m, kp, (int)cl, s) != 0) return cuda_fail(c);
+    c->last_launches = launches + 1;
+    return IVM_OK;
+  }
+  if (use_v3g(c, m)) {
     const void *tw;
     r = get_table3(c, m, prec, &tw);
     if (r) return r;

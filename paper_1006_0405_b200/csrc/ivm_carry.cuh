@@ -8,29 +8,33 @@
 // carry into word k is c_k = g_{k-1} | (p_{k-1} & c_{k-1}).  Inside a warp the
 // 32 carries of one step come from the ballot adder cin = ((G|P) + G + c0) ^ P
 // (bit l of the sum (G|P) + G + c0 is the carry into lane l, complemented where
-// P_l), across warps from one more ballot scan; the digits are the bytes of
-// (u_k + c_k) mod 2^32.  Lane l of warp w handles word k = w SEG + 32 j + l, so
-// the coefficient reads (16 B per lane) and the digit stores are contiguous.
+// P_l), across warps (and across the CTAs of a cluster) from the same adder on
+// the per-warp (per-CTA) generate / all-propagate bits; the digits are the
+// bytes of (u_k + c_k) mod 2^32.  Lane l of warp w handles word
+// k = k_begin + w 32 J + 32 j + l, so coefficient reads (16 B per lane) and the
+// digit stores are contiguous.
 #pragma once
 #include <stdint.h>
 
 namespace ivm {
 
-// word k of the split: (low 32 bits, high bits) of V_k; c_i = 0 outside [0, nc)
-static __device__ __forceinline__ void carry_word(const int32_t *coef, int nc, int k, unsigned &lo,
-                                                  unsigned &hi) {
+// word k of the split: (low 32 bits, high bits) of V_k; c_i = 0 outside [0, nc).
+// Src::quad(k) returns c_{4k .. 4k+3} (only called when 4k + 3 < nc);
+// Src::one(i) returns c_i.
+template <typename Src>
+static __device__ __forceinline__ void carry_word(const Src &src, int nc, int k, unsigned &lo, unsigned &hi) {
   if (k < 0 || 4 * k >= nc) {
     lo = hi = 0u;
     return;
   }
   unsigned c0, c1, c2, c3;
   if (4 * k + 3 < nc) {
-    const int4 q = reinterpret_cast<const int4 *>(coef)[k];
+    const int4 q = src.quad(k);
     c0 = (unsigned)q.x, c1 = (unsigned)q.y, c2 = (unsigned)q.z, c3 = (unsigned)q.w;
   } else {
-    c0 = (unsigned)coef[4 * k];
-    c1 = 4 * k + 1 < nc ? (unsigned)coef[4 * k + 1] : 0u;
-    c2 = 4 * k + 2 < nc ? (unsigned)coef[4 * k + 2] : 0u;
+    c0 = (unsigned)src.one(4 * k);
+    c1 = 4 * k + 1 < nc ? (unsigned)src.one(4 * k + 1) : 0u;
+    c2 = 4 * k + 2 < nc ? (unsigned)src.one(4 * k + 2) : 0u;
     c3 = 0u;
   }
   const unsigned long long v = (unsigned long long)c0 + ((unsigned long long)c1 << 8) +
@@ -39,6 +43,13 @@ static __device__ __forceinline__ void carry_word(const int32_t *coef, int nc, i
   hi = (unsigned)(v >> 32);
 }
 
+// a plain [nc] int32 array (16-byte aligned)
+struct CoefLinear {
+  const int32_t *c;
+  __device__ __forceinline__ int4 quad(int k) const { return reinterpret_cast<const int4 *>(c)[k]; }
+  __device__ __forceinline__ int one(int i) const { return c[i]; }
+};
+
 // per step: u (mod 2^32) and the generate / propagate bits of this lane's word.
 // hprev / eprev: hi_{k-1} and floor(W_{k-1} / 2^32) of the word below lane 0.
 struct CarryStep {
@@ -46,10 +57,11 @@ struct CarryStep {
   bool g, p;
   unsigned hi_top, ov_top;  // lane 31's hi and overflow, for the next step's lane 0
 };
-static __device__ __forceinline__ CarryStep carry_step(const int32_t *coef, int nc, int k, unsigned lane,
-                                                       unsigned hprev, unsigned eprev) {
+template <typename Src>
+static __device__ __forceinline__ CarryStep carry_step(const Src &src, int nc, int k, unsigned lane, unsigned hprev,
+                                                       unsigned eprev) {
   unsigned lo, hi;
-  carry_word(coef, nc, k, lo, hi);
+  carry_word(src, nc, k, lo, hi);
   unsigned hp = __shfl_up_sync(0xffffffffu, hi, 1);
   if (lane == 0) hp = hprev;
   const unsigned w = lo + hp;
@@ -65,71 +77,90 @@ static __device__ __forceinline__ CarryStep carry_step(const int32_t *coef, int 
   return s;
 }
 
-// coef: [2n-1] int32, 16-byte aligned (shared); out: [2n] digits (global).
-// Every thread of the block calls it (blockDim.x a multiple of 32, <= 1024).
-static __device__ __forceinline__ void carry_store(const int32_t *coef, int n, uint8_t *__restrict__ out,
-                                                   bool certified) {
-  const int nout = 2 * n, nc = 2 * n - 1;
-  if (!certified) {
-    for (int i = threadIdx.x; i < nout; i += blockDim.x) out[i] = 0;
-    return;
-  }
+// Carry over the words [kb, ke) of one CTA.  Phase 1 (carry_seg_scan): every
+// warp scans its sub-segment with carry-in 0; returns the CTA's generate (carry
+// out with carry-in 0) and all-propagate bits.  Phase 2 (carry_seg_emit): given
+// the CTA's carry-in, writes the digits of the words.  Every thread of the block
+// calls both (blockDim.x a multiple of 32, <= 1024); CarrySeg lives in shared memory.
+struct CarrySeg {
+  unsigned wg[32], wp[32];
+};
+template <typename Src>
+static __device__ __forceinline__ void carry_seg_scan(const Src &src, int nc, int kb, int ke, CarrySeg &cs,
+                                                      unsigned &gen, unsigned &allp) {
   const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  const int words = (nout + 3) / 4;
-  const int J = (words + 32 * (int)nwarps - 1) / (32 * (int)nwarps);  // steps per warp
-  const int k0 = (int)warp * 32 * J;
-  // the two words below the segment: hi_{k0-1}, floor(W_{k0-1} / 2^32)
-  unsigned hprev, eprev;
+  const int J = (ke - kb + 32 * (int)nwarps - 1) / (32 * (int)nwarps);
+  const int k0 = kb + (int)warp * 32 * J;
+  unsigned hp, ep;
   {
     unsigned l1, h1, l2, h2;
-    carry_word(coef, nc, k0 - 1, l1, h1);
-    carry_word(coef, nc, k0 - 2, l2, h2);
-    hprev = h1;
-    eprev = (l1 + h2) < l1 ? 1u : 0u;
+    carry_word(src, nc, k0 - 1, l1, h1);
+    carry_word(src, nc, k0 - 2, l2, h2);
+    hp = h1;
+    ep = (l1 + h2) < l1 ? 1u : 0u;
   }
-  // pass 1: the segment's generate (carry out with carry in 0) and all-propagate
   unsigned c = 0u;
-  bool allp = true;
-  {
-    unsigned hp = hprev, ep = eprev;
-    for (int j = 0; j < J; j++) {
-      const int k = k0 + 32 * j + (int)lane;
-      const CarryStep s = carry_step(coef, nc, k, lane, hp, ep);
-      const unsigned G = __ballot_sync(0xffffffffu, s.g), P = __ballot_sync(0xffffffffu, s.p);
-      const unsigned long long S = (unsigned long long)(G | P) + G + c;
-      c = (unsigned)(S >> 32);
-      allp = allp && (P == 0xffffffffu);
-      hp = s.hi_top;
-      ep = s.ov_top;
-    }
-  }
-  __shared__ unsigned wg[32], wp[32], wc[32];
-  if (lane == 0) {
-    wg[warp] = c;
-    wp[warp] = allp ? 1u : 0u;
-  }
-  __syncthreads();
-  if (warp == 0) {
-    const bool gg = lane < nwarps ? wg[lane] != 0 : false;
-    const bool pp = lane < nwarps ? wp[lane] != 0 : false;
-    const unsigned G2 = __ballot_sync(0xffffffffu, gg), P2 = __ballot_sync(0xffffffffu, pp);
-    const unsigned cin = ((G2 | P2) + G2) ^ P2;
-    if (lane < nwarps) wc[lane] = (cin >> lane) & 1u;
-  }
-  __syncthreads();
-  // pass 2: carries into every word, digits out
-  c = wc[warp];
-  const bool wide = (reinterpret_cast<uintptr_t>(out) & 3) == 0;
-  unsigned hp = hprev, ep = eprev;
+  bool ap = true;
   for (int j = 0; j < J; j++) {
     const int k = k0 + 32 * j + (int)lane;
-    const CarryStep s = carry_step(coef, nc, k, lane, hp, ep);
-    const unsigned G = __ballot_sync(0xffffffffu, s.g), P = __ballot_sync(0xffffffffu, s.p);
+    const CarryStep s = carry_step(src, nc, k, lane, hp, ep);
+    // words beyond the segment neither generate nor propagate
+    const bool in = k < ke;
+    const unsigned G = __ballot_sync(0xffffffffu, in && s.g), P = __ballot_sync(0xffffffffu, !in || s.p);
+    const unsigned long long S = (unsigned long long)(G | P) + G + c;
+    c = (unsigned)(S >> 32);
+    ap = ap && (P == 0xffffffffu);
+    hp = s.hi_top;
+    ep = s.ov_top;
+  }
+  if (lane == 0) {
+    cs.wg[warp] = c;
+    cs.wp[warp] = ap ? 1u : 0u;
+  }
+  __syncthreads();
+  unsigned G2 = 0, P2 = 0;
+  for (unsigned w = 0; w < nwarps; w++) {
+    G2 |= (cs.wg[w] != 0u ? 1u : 0u) << w;
+    P2 |= (cs.wp[w] != 0u ? 1u : 0u) << w;
+  }
+  const unsigned long long S = (unsigned long long)(G2 | P2) + G2;
+  gen = (unsigned)(S >> nwarps) & 1u;
+  allp = (nwarps == 32 ? P2 == 0xffffffffu : P2 == ((1u << nwarps) - 1u)) ? 1u : 0u;
+}
+
+template <typename Src>
+static __device__ __forceinline__ void carry_seg_emit(const Src &src, int nc, int nout, int kb, int ke,
+                                                      const CarrySeg &cs, unsigned cin, uint8_t *__restrict__ out) {
+  const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int J = (ke - kb + 32 * (int)nwarps - 1) / (32 * (int)nwarps);
+  const int k0 = kb + (int)warp * 32 * J;
+  unsigned G2 = 0, P2 = 0;
+  for (unsigned w = 0; w < nwarps; w++) {
+    G2 |= (cs.wg[w] != 0u ? 1u : 0u) << w;
+    P2 |= (cs.wp[w] != 0u ? 1u : 0u) << w;
+  }
+  const unsigned long long S0 = (unsigned long long)(G2 | P2) + G2 + cin;
+  unsigned c = (unsigned)((S0 ^ P2) >> warp) & 1u;  // carry into this warp's sub-segment
+  unsigned hp, ep;
+  {
+    unsigned l1, h1, l2, h2;
+    carry_word(src, nc, k0 - 1, l1, h1);
+    carry_word(src, nc, k0 - 2, l2, h2);
+    hp = h1;
+    ep = (l1 + h2) < l1 ? 1u : 0u;
+  }
+  const bool wide = (reinterpret_cast<uintptr_t>(out) & 3) == 0;
+  for (int j = 0; j < J; j++) {
+    const int k = k0 + 32 * j + (int)lane;
+    const CarryStep s = carry_step(src, nc, k, lane, hp, ep);
+    const bool in = k < ke;
+    const unsigned G = __ballot_sync(0xffffffffu, in && s.g), P = __ballot_sync(0xffffffffu, !in || s.p);
     const unsigned long long S = (unsigned long long)(G | P) + G + c;
     const unsigned cl = (((unsigned)S ^ P) >> lane) & 1u;
     c = (unsigned)(S >> 32);
     hp = s.hi_top;
     ep = s.ov_top;
+    if (!in) continue;
     const unsigned d = s.u + cl;
     const int i = 4 * k;
     if (i + 3 < nout && wide) {
@@ -140,6 +171,23 @@ static __device__ __forceinline__ void carry_store(const int32_t *coef, int n, u
         if (i + b < nout) out[i + b] = (uint8_t)(d >> (8 * b));
     }
   }
+}
+
+// whole product in one CTA.  coef: [2n-1] int32, 16-byte aligned (shared);
+// out: [2n] digits (global).  Uncertified pairs get zero digits.
+static __device__ __forceinline__ void carry_store(const int32_t *coef, int n, uint8_t *__restrict__ out,
+                                                   bool certified) {
+  const int nout = 2 * n, nc = 2 * n - 1;
+  if (!certified) {
+    for (int i = threadIdx.x; i < nout; i += blockDim.x) out[i] = 0;
+    return;
+  }
+  __shared__ CarrySeg seg;
+  const CoefLinear src{coef};
+  const int words = (nout + 3) / 4;
+  unsigned gen, allp;
+  carry_seg_scan(src, nc, 0, words, seg, gen, allp);
+  carry_seg_emit(src, nc, nout, 0, words, seg, 0u, out);
 }
 
 }  // namespace ivm

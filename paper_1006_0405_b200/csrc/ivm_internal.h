@@ -25,6 +25,8 @@ struct LaunchInfo {
   bool a_smem;
   size_t a_bytes_per_cta;
   int blocks_per_sm;
+  int cluster = 1;       // CTAs per multiplication (v4)
+  int max_clusters = 0;  // co-resident clusters (v4)
 };
 
 int upload_w32(const double *w64, const float *w32);
@@ -58,6 +60,12 @@ struct GroupArgs {
   unsigned *agg;
 };
 int v3g_info(int prec, int m, GroupInfo *gi);
+// m = 2^14 .. 2^16: one thread-block cluster of m/8192 CTAs per multiplication
+int upload_w64_v4(const double *w64, const float *w32);
+int v4_table_entries(int m);
+int v4_tables(int m, int prec, const void *w2N, void *out);
+int v4_info(int prec, int m, LaunchInfo *li);
+int v4_launch(int prec, int m, const KParams &kp, int clusters, cudaStream_t s);
 int v3g_launch(int prec, int m, const KParams &kp, const GroupArgs &ga, int grid, cudaStream_t s);
 
 }  // namespace ivm

@@ -101,15 +101,17 @@ template <int M, int R = 16> struct G3 {
     return c;
   }
   static constexpr int CAP = cap();
-  // twiddle table segment offsets (entries of CI<T>)
+  // twiddle table segment offsets (compact entries); every segment starts at an
+  // even entry so that bulk copies of segments are 16-byte aligned in fp32 too
+  __host__ __device__ static constexpr int even(int x) { return (x + 1) & ~1; }
   __host__ __device__ static constexpr int tw_fwd(int p) {  // p >= 1: [R-1][L/2]
     int o = 0;
-    for (int k = 1; k < p; k++) o += (plan_cta(M, R).f[k] - 1) * (fL(plan_cta(M, R), k) / 2);
+    for (int k = 1; k < p; k++) o += even((plan_cta(M, R).f[k] - 1) * (fL(plan_cta(M, R), k) / 2));
     return o;
   }
   __host__ __device__ static constexpr int tw_inv(int p) {  // p >= 1: [Q-1][L]
     int o = tw_fwd(plan_cta(M, R).nf);
-    for (int k = 1; k < p; k++) o += (plan_cta(M, R).q[k] - 1) * iL(plan_cta(M, R), k);
+    for (int k = 1; k < p; k++) o += even((plan_cta(M, R).q[k] - 1) * iL(plan_cta(M, R), k));
     return o;
   }
   __host__ __device__ static constexpr int tw_fin() { return tw_inv(plan_cta(M, R).ni); }  // [Q_last][L_last]
@@ -393,8 +395,9 @@ struct CertAcc {  // per-thread; reduced once per multiplication
   double rad = 0.0;
 };
 
+// coefficient i (global index) -> *dst (the snapped integer, or 0)
 template <typename T>
-__device__ __forceinline__ void certify_real(T lo, T hi, int i, int n, int32_t *coef, CertAcc &acc,
+__device__ __forceinline__ void certify_real(T lo, T hi, int i, int n, int32_t *dst, CertAcc &acc,
                                              double *dump) {
   if (dump) reinterpret_cast<double4 *>(dump)[i] = make_double4((double)lo, (double)hi, 0.0, 0.0);
   if (i >= 2 * n - 1) return;
@@ -403,7 +406,7 @@ __device__ __forceinline__ void certify_real(T lo, T hi, int i, int n, int32_t *
   const bool ok = cl == floor(h);
   const double rad = __dmul_ru(__dadd_ru(h, -l), 0.5);
   acc.rad = (rad <= acc.rad) ? acc.rad : rad;  // NaN propagates (comparison false)
-  coef[i] = ok ? (int32_t)cl : 0;
+  *dst = ok ? (int32_t)cl : 0;
   if (!ok) {
     acc.ok = 0;
     acc.bad = min(acc.bad, i);
@@ -436,20 +439,21 @@ __device__ __forceinline__ void emit_coeffs(const CI<T> &o, int k, const TwC<T> 
   constexpr int N = 1 << M;
   const CI<T> v = rtmul<T, true>(ldg_twc(tw, twi), o);  // z^{-k} = conj(z^k)
   const T s = T(2) / T(N);  // exact power of two
-  certify_real(DR<T>::mul_rd(v.rl, s), DR<T>::mul_ru(v.rh, s), k, n, coef, acc, dump);
-  certify_real(DR<T>::mul_rd(v.il, s), DR<T>::mul_ru(v.ih, s), k + N / 2, n, coef, acc, dump);
+  certify_real(DR<T>::mul_rd(v.rl, s), DR<T>::mul_ru(v.rh, s), k, n, coef + k, acc, dump);
+  certify_real(DR<T>::mul_rd(v.il, s), DR<T>::mul_ru(v.ih, s), k + N / 2, n, coef + k + N / 2, acc, dump);
 }
 
 // folded variant: the input twiddles already carried z^{-k0}; the remaining
 // factor z^{-L r} = conj(w_RATIO^r) (RATIO = 2m/L) is a compile-time constant
+// (c_k -> *d0, c_{k+m/2} -> *d1)
 template <typename T, int M, int RATIO>
-__device__ __forceinline__ void emit_fold(const CI<T> &o, int r, int k, int n, int32_t *coef, CertAcc &acc,
-                                          double *dump) {
+__device__ __forceinline__ void emit_fold(const CI<T> &o, int r, int k, int n, int32_t *d0, int32_t *d1,
+                                          CertAcc &acc, double *dump) {
   constexpr int N = 1 << M;
   const CI<T> v = ctw<T, true>(o, r, RATIO);
   const T s = T(2) / T(N);
-  certify_real(DR<T>::mul_rd(v.rl, s), DR<T>::mul_ru(v.rh, s), k, n, coef, acc, dump);
-  certify_real(DR<T>::mul_rd(v.il, s), DR<T>::mul_ru(v.ih, s), k + N / 2, n, coef, acc, dump);
+  certify_real(DR<T>::mul_rd(v.rl, s), DR<T>::mul_ru(v.rh, s), k, n, d0, acc, dump);
+  certify_real(DR<T>::mul_rd(v.il, s), DR<T>::mul_ru(v.ih, s), k + N / 2, n, d1, acc, dump);
 }
 
 template <typename T, int M, int RK>
@@ -763,7 +767,10 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
         __syncthreads();  // every input loaded: the coefficients may overwrite the state
         double *dump = diag_dump(kp, pair, N);
 #pragma unroll
-        for (int r = 0; r < R; r++) emit_fold<T, M, RATIO>(v[r], r, k0 + pp.L * r, n, coef, acc, dump);
+        for (int r = 0; r < R; r++) {
+          const int k = k0 + pp.L * r;
+          emit_fold<T, M, RATIO>(v[r], r, k, n, coef + k, coef + k + N / 2, acc, dump);
+        }
       } else {
         invR<T, R, false>(st, twb, pp, v, k0, nu);
         __syncthreads();

@@ -1,0 +1,377 @@
+// ivm_v4.cuh -- cluster kernel for m = 2^14 .. 2^16: one thread-block cluster of
+// C = m/8192 CTAs per multiplication, every CTA running the m = 8192 one-CTA
+// schedule of ivm_v3.cuh on its share (included by ivm_v4.cu).
+//
+// Row split of the odd-frequency transform (ivm_v3.cuh).  After the trivial
+// radix-2 pass, a first DIT pass of radix C gives the half-stored
+// rows k < C of level 2C; CTA c computes row c from the digits:
+//   G[c][v] = sum_q w_{4C}^{q(1+4r)} x[v + (m/2C) q],  r = c/2 (c even), or the
+//   conjugate of the r = (2C-1-c)/2 output (c odd, the mirrored row).
+// Every later forward pass maps row k0 to rows k0 + L r and their mirrors, so the
+// rows {k = c or 2C-1-c (mod 2C)} stay in CTA c: with local index kappa,
+//   k = C kappa + (kappa even ? c : C-1-c),
+// the local passes, storage and mirror rules are exactly the m = 8192 ones; only
+// the twiddle values w_{2LR}^{q(2k+1)} differ per CTA ("role" tables).  The
+// pointwise product and the inverse passes 0..3 are local too (the inverse rows
+// are the same in every CTA, the columns are the CTA's classes); the last inverse
+// pass (radix C, untwist z^{-k} folded into its input twiddles) combines one
+// column from every CTA: it reads them through distributed shared memory.  The
+// coefficients stay in the producing CTA's shared memory; the carry runs over
+// contiguous word segments with the cluster-level ballot adder.
+#pragma once
+
+namespace ivm {
+namespace v4 {
+
+using namespace v3;
+
+template <int M> struct G4 {
+  static_assert(M >= 14 && M <= 16, "cluster sizes 2, 4, 8");
+  static constexpr int C = 1 << (M - 13);
+  static constexpr int B = 4096 / C;  // rows of the last inverse pass per CTA
+  static constexpr int LGB = 12 - (M - 13);
+  using GL = G3<13, 8>;  // the local (m = 8192) layout
+  // device table (compact entries of 2 T):
+  //   FWD(c): role c, local forward passes 1..4 at FP(p) = 0, 7, 63, 512 ([R-1][L/2] each;
+  //           pass 4 starts at an even entry so every bulk copy is 16-byte aligned in fp32 too)
+  //   INV:    local inverse passes 1..3: [7][8], [7][64], [7][512] (shared)
+  //   XINV(c): role c, last inverse pass, [C][B] (rows c B .. c B + B - 1), folded untwist
+  //   TH(c):  role c, theta_q (q < C) as full intervals (2 entries each)
+  __host__ __device__ static constexpr int FWD(int c) { return c * 4096; }
+  __host__ __device__ static constexpr int FP(int p) { return p == 1 ? 0 : (p == 2 ? 7 : (p == 3 ? 63 : 512)); }
+  static constexpr int INV = C * 4096;
+  static constexpr int INV1 = 0, INV2 = 56, INV3 = 504, INV_ENT = 4088;
+  __host__ __device__ static constexpr int XINV(int c) { return INV + 4096 + c * 4096; }
+  __host__ __device__ static constexpr int TH(int c) { return INV + 4096 + C * 4096 + 2 * C * c; }
+  static constexpr int TOTAL = INV + 4096 + C * 4096 + 2 * C * C;
+  // shared-memory twiddle area (entries)
+  static constexpr int S_SWAP = 0;          // 4096: forward-last -> inverse pass 3 -> last inverse pass
+  static constexpr int S_MF = 4096;         // forward passes 1..3 (511 entries + 1 pad)
+  static constexpr int S_MI = 4096 + 512;   // inverse passes 1, 2 (504 entries)
+  static constexpr int S_TH = 4096 + 1016;  // theta (2C entries)
+  static constexpr int S_ENT = S_TH + 2 * C;
+  static constexpr int FLAST = 3584, MF_ENT = 512, MI_ENT = 504;
+};
+
+template <int M> struct RT4 {
+  using GL = G3<13, 8>;
+  __host__ __device__ static constexpr PassRT fwd(int i) {  // local forward pass p = i + 1
+    return PassRT{ilog2r(8192 / fL(plan_cta(13, 8), i + 1) / 8), fL(plan_cta(13, 8), i + 1), GL::fRS(i + 1),
+                  (i + 2 < 5) ? GL::fRS(i + 2) : GL::iRS(1), GL::fSW(i + 1), (i + 2 < 5) ? GL::fSW(i + 2) : GL::iSW(1),
+                  (i < 3) ? G4<M>::S_MF + G4<M>::FP(i + 1) : G4<M>::S_SWAP, (i == 3) ? 1 : 0, 0};
+  }
+  __host__ __device__ static constexpr PassRT inv(int i) {  // local inverse pass p = i + 1 (unfolded)
+    return PassRT{ilog2r(8192 / iL(plan_cta(13, 8), i + 1) / 8), iL(plan_cta(13, 8), i + 1), GL::iRS(i + 1),
+                  GL::iRS(i + 2), GL::iSW(i + 1), GL::iSW(i + 2),
+                  (i == 0) ? G4<M>::S_MI : (i == 1 ? G4<M>::S_MI + 56 : G4<M>::S_SWAP), (i == 2) ? 1 : 0, 0};
+  }
+};
+template <int M> __device__ __forceinline__ PassRT pick_fwd4(int i) {
+  constexpr PassRT p0 = RT4<M>::fwd(0), p1 = RT4<M>::fwd(1), p2 = RT4<M>::fwd(2), p3 = RT4<M>::fwd(3);
+  return i == 0 ? p0 : (i == 1 ? p1 : (i == 2 ? p2 : p3));
+}
+template <int M> __device__ __forceinline__ PassRT pick_inv4(int i) {
+  constexpr PassRT p0 = RT4<M>::inv(0), p1 = RT4<M>::inv(1), p2 = RT4<M>::inv(2);
+  return i == 0 ? p0 : (i == 1 ? p1 : p2);
+}
+
+// ---- cluster primitives ----
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned dsm_map(const void *p, unsigned cta) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(cta));
+  return r;
+}
+__device__ __forceinline__ unsigned dsm_map_addr(unsigned a, unsigned cta) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(cta));
+  return r;
+}
+__device__ __forceinline__ double2 dsm_ld(unsigned a, double2 *) {
+  double2 v;
+  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ float2 dsm_ld(unsigned a, float2 *) {
+  float2 v;
+  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ int4 dsm_ld_i4(unsigned a) {
+  int4 v;
+  asm volatile("ld.shared::cluster.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ int dsm_ld_i32(unsigned a) {
+  int v;
+  asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long dsm_ld_u64(unsigned a) {
+  unsigned long long v;
+  asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+  return v;
+}
+
+// coefficients of the cluster: c_i lives in the CTA that owns row
+// k0 = (i mod m/2) mod 4096 of the last inverse pass, at local index
+// (h C + r) B + (k0 - p B), i = h m/2 + r 4096 + k0, p = k0 / B
+template <int M> struct CoefCluster {
+  unsigned base;  // shared::cta address of the local coefficient array
+  __device__ __forceinline__ unsigned addr(int i) const {
+    using X = G4<M>;
+    constexpr int HALF = (1 << M) / 2;
+    const int h = i >= HALF ? 1 : 0;
+    const int ii = i - h * HALF;
+    const int r = ii >> 12, k0 = ii & 4095, p = k0 >> X::LGB;
+    const int idx = (h * X::C + r) * X::B + (k0 - (p << X::LGB));
+    return dsm_map_addr(base + 4u * (unsigned)idx, (unsigned)p);
+  }
+  __device__ __forceinline__ int4 quad(int k) const { return dsm_ld_i4(addr(4 * k)); }
+  __device__ __forceinline__ int one(int i) const { return dsm_ld_i32(addr(i)); }
+};
+
+// first (cross-CTA) forward pass from the digits: row `crank` of level 2C,
+// 4096 columns; x >= 0 is a point, so [x th.lo, x th.hi] needs no sign cases
+template <typename T, int M>
+__device__ __forceinline__ void cross_fwd(const uint8_t *__restrict__ dig, int n, Buf<T> st, const CI<T> *theta,
+                                          unsigned crank) {
+  constexpr int C = G4<M>::C;
+  const int t = threadIdx.x;
+  CI<T> acc[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) acc[j] = CI<T>{T(0), T(0), T(0), T(0)};
+#pragma unroll
+  for (int q = 0; q < C; q++) {
+    const CI<T> th = theta[q];
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      const int idx = t + 512 * j + 4096 * q;
+      const T x = idx < n ? T(dig[idx]) : T(0);
+      acc[j].rl = DR<T>::fma_rd(x, th.rl, acc[j].rl);
+      acc[j].rh = DR<T>::fma_ru(x, th.rh, acc[j].rh);
+      acc[j].il = DR<T>::fma_rd(x, th.il, acc[j].il);
+      acc[j].ih = DR<T>::fma_ru(x, th.ih, acc[j].ih);
+    }
+  }
+  const bool odd = (crank & 1u) != 0u;
+#pragma unroll
+  for (int j = 0; j < 8; j++) st.st(t + 512 * j, odd ? cconj(acc[j]) : acc[j]);
+}
+
+template <typename T, int M> struct Cfg4 {
+  using GL = G3<13, 8>;
+  static constexpr int THREADS = 512;
+  static constexpr size_t E = sizeof(typename V2t<T>::t);
+  static constexpr size_t STATE_BYTES = 2 * E * (size_t)GL::CAP;
+  static constexpr size_t TW_BYTES = sizeof(TwC<T>) * (size_t)G4<M>::S_ENT;
+  static constexpr size_t SMEM = STATE_BYTES + TW_BYTES;
+  static constexpr size_t A_BYTES = 2 * E * 4096;
+  static_assert(STATE_BYTES >= 4 * 8192, "local coefficients alias the state");
+  static_assert(SMEM <= 227 * 1024, "shared memory");
+};
+
+template <typename T, int M>
+__global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
+  using X = G4<M>;
+  using GL = G3<13, 8>;
+  using CF = Cfg4<T, M>;
+  using V = typename V2t<T>::t;
+  constexpr int C = X::C, B = X::B, R = 8, NL = 8192, N = 1 << M;
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ Cert3 cs;
+  __shared__ CarrySeg seg;
+  __shared__ unsigned s_link[2];
+  __shared__ __align__(8) unsigned long long tbar;
+  Buf<T> st{reinterpret_cast<V *>(smem), reinterpret_cast<V *>(smem) + GL::CAP};
+  int32_t *coefL = reinterpret_cast<int32_t *>(smem);  // [2][C][B], aliases the state
+  TwC<T> *twb = reinterpret_cast<TwC<T> *>(smem + CF::STATE_BYTES);
+  const CI<T> *theta = reinterpret_cast<const CI<T> *>(twb + X::S_TH);
+  const unsigned crank = cluster_rank();
+  const int cid = (int)(blockIdx.x / C), ncl = (int)(gridDim.x / C);
+  const TwC<T> *tw = reinterpret_cast<const TwC<T> *>(kp.tw);
+  Buf<T> A{reinterpret_cast<V *>(kp.ascratch) + (size_t)blockIdx.x * NL, nullptr};
+  A.im = A.re + NL / 2;
+  const int n = kp.n, nc = 2 * n - 1, nout = 2 * n;
+  constexpr int RSI1 = GL::iRS(1), SWI1 = GL::iSW(1);
+  constexpr unsigned EB = sizeof(TwC<T>);
+
+  if (threadIdx.x == 0) mbar_init(&tbar);
+  __syncthreads();
+  if (threadIdx.x == 0 && cid < kp.batch) {
+    mbar_expect(&tbar, EB * (X::FLAST + X::MF_ENT + X::MI_ENT + 2 * C));
+    bulk_copy(twb + X::S_SWAP, tw + X::FWD(crank) + X::FP(4), EB * X::FLAST, &tbar);
+    bulk_copy(twb + X::S_MF, tw + X::FWD(crank), EB * X::MF_ENT, &tbar);
+    bulk_copy(twb + X::S_MI, tw + X::INV, EB * X::MI_ENT, &tbar);
+    bulk_copy(twb + X::S_TH, tw + X::TH(crank), EB * 2 * C, &tbar);
+  }
+  if (cid < kp.batch) mbar_wait(&tbar, 0);
+  // tbar phases per pair it: 3 it (forward-last), 3 it + 1 (inverse pass 3),
+  // 3 it + 2 (last inverse pass) -> parities it&1, (it+1)&1, it&1
+
+  int it = 0;
+  for (int pair = cid; pair < kp.batch; pair += ncl, it++) {
+    const unsigned par = (unsigned)it & 1u;
+#pragma unroll 1
+    for (int op = 0; op < 2; op++) {
+      cross_fwd<T, M>((op == 0 ? kp.a : kp.b) + (size_t)pair * n, n, st, theta, crank);
+      if (op == 1 && threadIdx.x == 0) {
+        cs.ok = 1;
+        cs.first_bad = 0x7fffffff;
+        cs.maxrad = 0ull;
+      }
+      __syncthreads();
+#pragma unroll 1
+      for (int i = 0; i < 4; i++) {
+        const PassRT pp = pick_fwd4<M>(i);
+        CI<T> v[R];
+        int k0, nu;
+        if (op == 0 && i == 3) mbar_wait(&tbar, par);  // forward-last table of this role
+        fwdR<T, R>(st, twb, pp, v, k0, nu);
+        if (i < 3) {
+          __syncthreads();
+#pragma unroll
+          for (int r = 0; r < R; r++) {
+            if (2 * r < R) st.st(sidx(k0 + pp.L * r, nu, pp.RSo, pp.SWo), v[r]);
+            else st.st(sidx(R * pp.L - 1 - k0 - pp.L * r, nu, pp.RSo, pp.SWo), cconj(v[r]));
+          }
+        } else if (op == 0) {
+#pragma unroll
+          for (int r = 0; r < R; r++) A.st(r * (pp.L >> 1) + k0, v[r]);
+        } else {  // last forward pass of b + pointwise + inverse pass 0
+          CI<T> an = A.ld(k0);
+#pragma unroll
+          for (int r = 0; r < R; r++) {
+            const CI<T> a = an;
+            if (r + 1 < R) an = A.ld((r + 1) * (pp.L >> 1) + k0);
+            v[r] = cmul(a, v[r]);
+          }
+          cdft<T, R, true>(v);
+          __syncthreads();
+          if (threadIdx.x == 0) {  // inverse pass 3 table replaces the forward-last one
+            mbar_expect(&tbar, EB * X::FLAST);
+            bulk_copy(twb + X::S_SWAP, tw + X::INV + X::INV3, EB * X::FLAST, &tbar);
+          }
+#pragma unroll
+          for (int r = 0; r < R; r++) st.st(sidx(r, k0, RSI1, SWI1), v[r]);
+        }
+        __syncthreads();
+      }
+    }
+    CertAcc acc;
+#pragma unroll 1
+    for (int i = 0; i < 3; i++) {
+      const PassRT pp = pick_inv4<M>(i);
+      CI<T> v[R];
+      int k0, nu;
+      if (i == 2) mbar_wait(&tbar, par ^ 1u);
+      invR<T, R, false>(st, twb, pp, v, k0, nu);
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < R; r++) st.st(sidx(k0 + pp.L * r, nu, pp.RSo, pp.SWo), v[r]);
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {  // last inverse pass table (this role's rows)
+      mbar_expect(&tbar, EB * 4096);
+      bulk_copy(twb + X::S_SWAP, tw + X::XINV(crank), EB * 4096, &tbar);
+    }
+    cluster_sync();  // (1) every CTA's column of the 4096 rows is in its shared memory
+    {
+      constexpr int G = 8 / C;  // rows (tasks) per thread
+      CI<T> v[G][C];
+      const unsigned re0 = (unsigned)__cvta_generic_to_shared(st.re), im0 = (unsigned)__cvta_generic_to_shared(st.im);
+#pragma unroll
+      for (int g = 0; g < G; g++) {
+        const int k0 = (int)crank * B + (int)threadIdx.x + 512 * g;
+#pragma unroll
+        for (int q = 0; q < C; q++) {
+          const unsigned src = (2 * q < C) ? (unsigned)(2 * q) : (unsigned)(2 * C - 1 - 2 * q);
+          const V r = dsm_ld(dsm_map_addr(re0 + (unsigned)(sizeof(V) * k0), src), (V *)nullptr);
+          const V m = dsm_ld(dsm_map_addr(im0 + (unsigned)(sizeof(V) * k0), src), (V *)nullptr);
+          const CI<T> z{r.x, r.y, m.x, m.y};
+          v[g][q] = (2 * q < C) ? z : cconj(z);
+        }
+      }
+      cluster_sync();  // (2) remote reads done: the state may be overwritten
+      mbar_wait(&tbar, par);
+      double *dump = diag_dump(kp, pair, N);
+#pragma unroll
+      for (int g = 0; g < G; g++) {
+        const int kl = (int)threadIdx.x + 512 * g, k0 = (int)crank * B + kl;
+#pragma unroll
+        for (int q = 0; q < C; q++) {
+          const TwC<T> w = twb[X::S_SWAP + q * B + kl];
+          v[g][q] = (2 * q < C) ? rtmul<T, true, true>(w, v[g][q]) : rtmul<T, false, true>(w, v[g][q]);
+        }
+        cdft<T, C, true>(v[g]);
+#pragma unroll
+        for (int r = 0; r < C; r++)
+          emit_fold<T, M, 4 * C>(v[g][r], r, k0 + 4096 * r, n, coefL + r * B + kl, coefL + (C + r) * B + kl, acc,
+                                 dump);
+      }
+    }
+    cert_flush(acc, cs);
+    __syncthreads();
+    if (threadIdx.x == 0 && pair + ncl < kp.batch) {  // next pair's forward-last table
+      mbar_expect(&tbar, EB * X::FLAST);
+      bulk_copy(twb + X::S_SWAP, tw + X::FWD(crank) + X::FP(4), EB * X::FLAST, &tbar);
+    }
+    cluster_sync();  // (3) coefficients and per-CTA certificates complete
+    int ok = 1, bad = 0x7fffffff;
+    unsigned long long rad = 0ull;
+#pragma unroll
+    for (int p = 0; p < C; p++) {
+      ok &= dsm_ld_i32(dsm_map(&cs.ok, (unsigned)p));
+      bad = min(bad, dsm_ld_i32(dsm_map(&cs.first_bad, (unsigned)p)));
+      const unsigned long long rp = dsm_ld_u64(dsm_map(&cs.maxrad, (unsigned)p));
+      rad = rp > rad ? rp : rad;
+    }
+    const int words = (nout + 3) / 4, wc = (words + C - 1) / C;
+    const int kb = min((int)crank * wc, words), ke = min(kb + wc, words);
+    uint8_t *out = kp.prod + (size_t)pair * nout;
+    const CoefCluster<M> src{(unsigned)__cvta_generic_to_shared(coefL)};
+    unsigned gen = 0u, allp = 1u;
+    if (ok) carry_seg_scan(src, nc, kb, ke, seg, gen, allp);
+    if (threadIdx.x == 0) {
+      s_link[0] = gen;
+      s_link[1] = allp;
+    }
+    cluster_sync();  // (4) per-CTA generate / all-propagate published
+    if (ok) {
+      unsigned Gc = 0u, Pc = 0u;
+#pragma unroll
+      for (int p = 0; p < C; p++) {
+        Gc |= (dsm_ld_i32(dsm_map(&s_link[0], (unsigned)p)) != 0 ? 1u : 0u) << p;
+        Pc |= (dsm_ld_i32(dsm_map(&s_link[1], (unsigned)p)) != 0 ? 1u : 0u) << p;
+      }
+      const unsigned cin = ((((Gc | Pc) + Gc) ^ Pc) >> crank) & 1u;
+      carry_seg_emit(src, nc, nout, kb, ke, seg, cin, out);
+    } else {
+      for (int i = 4 * kb + (int)threadIdx.x; i < min(4 * ke, nout); i += blockDim.x) out[i] = 0;
+    }
+    if (kp.coeffs) {
+      int64_t *co = kp.coeffs + (size_t)pair * nc;
+      for (int i = 4 * kb + (int)threadIdx.x; i < min(4 * ke, nc); i += blockDim.x) co[i] = ok ? src.one(i) : 0;
+    }
+    if (crank == 0 && threadIdx.x == 0) {
+      kp.cert[pair] = ok ? 1 : 0;
+      if (kp.max_radius) kp.max_radius[pair] = __longlong_as_double((long long)rad);
+      if (kp.first_bad) kp.first_bad[pair] = ok ? -1 : bad;
+    }
+    cluster_sync();  // (5) remote coefficient reads done before the next pair overwrites them
+  }
+}
+
+}  // namespace v4
+}  // namespace ivm

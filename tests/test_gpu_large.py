@@ -22,7 +22,7 @@ def ctx():
     return ivm.Context(0)
 
 
-@pytest.mark.parametrize("n", [4097, 8192, 8193, 12000, 16384, 30000])
+@pytest.mark.parametrize("n", [4097, 8192, 8193, 12000, 16384, 30000, 40000])
 def test_f64_large_sizes(ctx, n):
     kinds = np.array([0, 1, 2, 3])
     a, b = inputs.pair_digits(0xB16 + n, np.arange(4), n, kinds)

@@ -199,6 +199,27 @@ def test_host_entry_point_chunked_pipeline(ctx, n, batch):
     assert np.array_equal(out.numpy()[idx], oracle.long_multiply(a[idx], b[idx]))
 
 
+@pytest.mark.parametrize("n", [513, 1000, 1500, 2048, 3000, 4096])
+def test_f32_cta_sizes_never_wrong(ctx, n):
+    """fp32 through the one-CTA kernel (m = 2^10 .. 2^13): far past the fp32
+    limit, so pairs are mostly uncertified -- but a certified product must be
+    exact and an uncertified one all zeros, and the dumped intervals must still
+    contain the exact coefficients."""
+    a, b = inputs.pair_digits(0xF3 + n, np.arange(4), n, np.array([0, 1, 2, 3]))
+    g = gpu_run(ctx, a, b, prec="f32", dump=[0, 1])
+    want = oracle.long_multiply(a, b)
+    exact = oracle.coefficients(a[:2], b[:2])
+    for p in range(4):
+        if g["cert"][p]:
+            assert np.array_equal(g["prod"][p], want[p])
+        else:
+            assert not g["prod"][p].any()
+    for j in range(2):
+        iv = g["intervals"][j]
+        c = exact[j].astype(np.float64)
+        assert np.all(iv[:2 * n - 1, 0] <= c) and np.all(c <= iv[:2 * n - 1, 1])
+
+
 def test_argument_errors(ctx):
     import torch
     import paper_1006_0405_b200 as ivm
