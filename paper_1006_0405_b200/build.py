@@ -24,7 +24,8 @@ CXXFLAGS = ["-O2", "-fPIC", "-std=gnu++17", "-fext-numeric-literals", "-I", os.p
 
 CU = ["ivm_kernels.cu", "ivm_v3.cu", "ivm_v4.cu", "ivm_api.cu"]
 CPP = ["ivm_planner.cpp"]
-HDR = ["ivm_interval.cuh", "ivm_fft.cuh", "ivm_internal.h", "ivm_carry.cuh", "ivm_v3.cuh"]
+# every header under csrc/ is a dependency of every translation unit
+HDR = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 
 
 def _stale(obj: str, src: str) -> bool:

@@ -176,7 +176,10 @@ template <typename T, int M> struct Cfg4 {
   static constexpr size_t E = sizeof(typename V2t<T>::t);
   static constexpr size_t STATE_BYTES = 2 * E * (size_t)GL::CAP;
   static constexpr size_t TW_BYTES = sizeof(TwC<T>) * (size_t)G4<M>::S_ENT;
-  static constexpr size_t SMEM = STATE_BYTES + TW_BYTES;
+  // one operand's digits (n <= m/2 bytes), staged by a bulk copy one step ahead
+  // when it fits (m <= 2^15); else read from L2/HBM with an L2 prefetch
+  static constexpr size_t DIG_BYTES = STATE_BYTES + TW_BYTES + (size_t)(1 << M) / 2 <= 227 * 1024 ? (1 << M) / 2 : 0;
+  static constexpr size_t SMEM = STATE_BYTES + TW_BYTES + DIG_BYTES;
   static constexpr size_t A_BYTES = 2 * E * 4096;
   static_assert(STATE_BYTES >= 4 * 8192, "local coefficients alias the state");
   static_assert(SMEM <= 227 * 1024, "shared memory");
@@ -193,11 +196,12 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
   __shared__ Cert3 cs;
   __shared__ CarrySeg seg;
   __shared__ unsigned s_link[2];
-  __shared__ __align__(8) unsigned long long tbar;
+  __shared__ __align__(8) unsigned long long tbar, dbar;
   Buf<T> st{reinterpret_cast<V *>(smem), reinterpret_cast<V *>(smem) + GL::CAP};
   int32_t *coefL = reinterpret_cast<int32_t *>(smem);  // [2][C][B], aliases the state
   TwC<T> *twb = reinterpret_cast<TwC<T> *>(smem + CF::STATE_BYTES);
   const CI<T> *theta = reinterpret_cast<const CI<T> *>(twb + X::S_TH);
+  uint8_t *sdig = smem + CF::STATE_BYTES + CF::TW_BYTES;
   const unsigned crank = cluster_rank();
   const int cid = (int)(blockIdx.x / C), ncl = (int)(gridDim.x / C);
   const TwC<T> *tw = reinterpret_cast<const TwC<T> *>(kp.tw);
@@ -207,7 +211,12 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
   constexpr int RSI1 = GL::iRS(1), SWI1 = GL::iSW(1);
   constexpr unsigned EB = sizeof(TwC<T>);
 
-  if (threadIdx.x == 0) mbar_init(&tbar);
+  const bool staged = CF::DIG_BYTES > 0 && n % 16 == 0 &&
+                      ((reinterpret_cast<uintptr_t>(kp.a) | reinterpret_cast<uintptr_t>(kp.b)) % 16) == 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&tbar);
+    mbar_init(&dbar);
+  }
   __syncthreads();
   if (threadIdx.x == 0 && cid < kp.batch) {
     mbar_expect(&tbar, EB * (X::FLAST + X::MF_ENT + X::MI_ENT + 2 * C));
@@ -215,6 +224,10 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
     bulk_copy(twb + X::S_MF, tw + X::FWD(crank), EB * X::MF_ENT, &tbar);
     bulk_copy(twb + X::S_MI, tw + X::INV, EB * X::MI_ENT, &tbar);
     bulk_copy(twb + X::S_TH, tw + X::TH(crank), EB * 2 * C, &tbar);
+    if (staged) {  // operand a of the first pair (dbar phases: a = even, b = odd)
+      mbar_expect(&dbar, (unsigned)n);
+      bulk_copy(sdig, kp.a + (size_t)cid * n, (unsigned)n, &dbar);
+    }
   }
   if (cid < kp.batch) mbar_wait(&tbar, 0);
   // tbar phases per pair it: 3 it (forward-last), 3 it + 1 (inverse pass 3),
@@ -223,15 +236,31 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
   int it = 0;
   for (int pair = cid; pair < kp.batch; pair += ncl, it++) {
     const unsigned par = (unsigned)it & 1u;
+    if (!staged && pair + ncl < kp.batch) {  // L2 prefetch of the next pair's digits (this CTA's slice)
+      const int nxt = pair + ncl, sl = (n + C - 1) / C;
+      for (int off = (int)crank * sl + (int)threadIdx.x * 128; off < min(n, ((int)crank + 1) * sl);
+           off += (int)blockDim.x * 128) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(kp.a + (size_t)nxt * n + off));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(kp.b + (size_t)nxt * n + off));
+      }
+    }
 #pragma unroll 1
     for (int op = 0; op < 2; op++) {
-      cross_fwd<T, M>((op == 0 ? kp.a : kp.b) + (size_t)pair * n, n, st, theta, crank);
+      if (staged) mbar_wait(&dbar, (unsigned)op);
+      cross_fwd<T, M>(staged ? sdig : (op == 0 ? kp.a : kp.b) + (size_t)pair * n, n, st, theta, crank);
       if (op == 1 && threadIdx.x == 0) {
         cs.ok = 1;
         cs.first_bad = 0x7fffffff;
         cs.maxrad = 0ull;
       }
       __syncthreads();
+      if (staged && threadIdx.x == 0) {  // the next operand: b of this pair, or a of the next
+        const uint8_t *nx = op == 0 ? kp.b + (size_t)pair * n : kp.a + (size_t)(pair + ncl) * n;
+        if (op == 0 || pair + ncl < kp.batch) {
+          mbar_expect(&dbar, (unsigned)n);
+          bulk_copy(sdig, nx, (unsigned)n, &dbar);
+        }
+      }
 #pragma unroll 1
       for (int i = 0; i < 4; i++) {
         const PassRT pp = pick_fwd4<M>(i);
