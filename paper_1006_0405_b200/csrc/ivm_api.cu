@@ -25,7 +25,7 @@ struct ivm_ctx {
   std::map<std::pair<int, int>, ivm::LaunchInfo> info;
   std::map<std::pair<int, int>, ivm::LaunchInfo> info3;
   bool force_v1 = false;
-  bool force_v3g = false;  // IVM_KERNEL=v3g: the global-memory group kernel for m = 2^14 .. 2^16 too
+  bool force_v3g = false;  // IVM_KERNEL=v3g: the older global-state group kernel for every m >= 2^14
   std::map<std::pair<int, int>, void *> tw4;  // (log2m, prec) -> v4 role tables
   std::map<std::pair<int, int>, ivm::LaunchInfo> info4;
   int radix = 8;  // radix of the one-CTA kernel
@@ -113,7 +113,8 @@ int ivm_create(ivm_ctx_t *ctx, int device) {
       delete c;
       return IVM_EUNSUPPORTED;
     }
-    if (ivm::upload_w64(t64, t32) != 0 || ivm::upload_w64_v4(t64, t32) != 0) {
+    if (ivm::upload_w64(t64, t32) != 0 || ivm::upload_w64_v4(t64, t32) != 0 ||
+        ivm::upload_w64_v5(t64, t32) != 0) {
       delete c;
       return IVM_ECUDA;
     }
@@ -166,7 +167,22 @@ static int get_table(ivm_ctx_t c, int m, int prec, const void **out) {
 
 static bool use_v3(ivm_ctx_t c, int m) { return !c->force_v1 && m >= 10 && m <= 13; }
 static bool use_v4(ivm_ctx_t c, int m) { return !c->force_v3g && m >= 14 && m <= 16; }
-static bool use_v3g(ivm_ctx_t c, int m) { return m >= 14 && m <= 18 && !use_v4(c, m); }
+static bool use_v5(ivm_ctx_t c, int m) { return !c->force_v3g && (m == 17 || m == 18); }
+static bool use_v3g(ivm_ctx_t c, int m) { return m >= 14 && m <= 18 && !use_v4(c, m) && !use_v5(c, m); }
+
+static int get_info5(ivm_ctx_t c, int m, int prec, ivm::LaunchInfo *li) {
+  auto key = std::make_pair(m + 100, prec);
+  auto it = c->info4.find(key);
+  if (it != c->info4.end()) {
+    *li = it->second;
+    return IVM_OK;
+  }
+  int r = ivm::v5_info(prec, m, li);
+  if (r == -4) return IVM_EUNSUPPORTED;
+  if (r != 0 || li->blocks_per_sm < 1) return cuda_fail(c);
+  c->info4[key] = *li;
+  return IVM_OK;
+}
 
 static int get_table4(ivm_ctx_t c, int m, int prec, const void **out) {
   auto key = std::make_pair(m, prec);
@@ -302,6 +318,13 @@ int ivm_reserve(ivm_ctx_t c, size_t n, size_t batch, int prec) {
     size_t cl = (size_t)li.max_clusters < batch ? (size_t)li.max_clusters : batch;
     return ensure_scratch(c, cl * li.cluster * li.a_bytes_per_cta);
   }
+  if (use_v5(c, m)) {
+    const void *t4;
+    ivm::LaunchInfo li;
+    int r = get_table4(c, m, prec, &t4);
+    if (!r) r = get_info5(c, m, prec, &li);
+    return r;
+  }
   if (use_v3g(c, m)) {
     const void *t3;
     return get_table3(c, m, prec, &t3);
@@ -368,6 +391,43 @@ int ivm_multiply_batched_diag(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, s
     kp.ascratch = c->ascratch;
     kp.tw = tw;
     if (ivm::v4_launch(prec, m, kp, (int)cl, s) != 0) return cuda_fail(c);
+    c->last_launches = launches + 1;
+    return IVM_OK;
+  }
+  if (use_v5(c, m)) {
+    const void *tw;
+    ivm::LaunchInfo li;
+    r = get_table4(c, m, prec, &tw);
+    if (!r) r = get_info5(c, m, prec, &li);
+    if (r) return r;
+    const size_t C = (size_t)li.cluster;
+    size_t groups = (size_t)c->sms * li.blocks_per_sm / C;
+    if (groups > batch) groups = batch;
+    if (groups < 1) return IVM_EUNSUPPORTED;
+    r = ensure_scratch(c, groups * C * li.a_bytes_per_cta);
+    if (r) return r;
+    const size_t al = 256, M2 = (size_t)1 << m, es = prec == IVM_F64 ? 8 : 4;
+    auto up = [&](size_t x) { return (x + al - 1) / al * al; };
+    const size_t b_x = up(groups * C * 4096 * 4 * es), b_c = up(groups * M2 * 8), b_l = up(groups * C * 32),
+                 b_ctr = up(groups * 4);
+    const size_t need = b_x + b_c + b_l + b_ctr;
+    if (c->gscratch_bytes < need) {
+      cudaFree(c->gscratch);
+      c->gscratch = nullptr;
+      c->gscratch_bytes = 0;
+      if (cudaMalloc(&c->gscratch, need) != cudaSuccess) return IVM_ENOMEM;
+      c->gscratch_bytes = need;
+    }
+    char *gs = (char *)c->gscratch;
+    ivm::Group5Args ga;
+    ga.xch = gs;
+    ga.coef = (long long *)(gs + b_x);
+    ga.link = (unsigned *)(gs + b_x + b_c);
+    ga.ctr = (unsigned *)(gs + b_x + b_c + b_l);
+    if (cudaMemsetAsync(ga.ctr, 0, b_ctr, s) != cudaSuccess) return cuda_fail(c);
+    kp.ascratch = c->ascratch;
+    kp.tw = tw;
+    if (ivm::v5_launch(prec, m, kp, ga, (int)groups, s) != 0) return cuda_fail(c);
     c->last_launches = launches + 1;
     return IVM_OK;
   }

@@ -1,7 +1,7 @@
 // ivm_carry.cuh -- carry of snapped coefficients to base-256 digits.
 //
 // Word form of the carry.  Four digit positions make one 32-bit word:
-//   V_k = sum_{b<4} c_{4k+b} 256^b  (< 2^56 for 0 <= c_i < 2^31),  sum_i c_i 256^i = sum_k V_k 2^{32k}.
+//   V_k = sum_{b<4} c_{4k+b} 256^b  (< 2^58 for 0 <= c_i < 2^33),  sum_i c_i 256^i = sum_k V_k 2^{32k}.
 // With V_k = lo_k + hi_k 2^32 the word sums W_k = lo_k + hi_{k-1} < 2^33 and
 // u_k = (W_k mod 2^32) + floor(W_{k-1} / 2^32) <= 2^32 leave carries of 0 or 1:
 // generate g_k = (u_k == 2^32), propagate p_k = (u_k == 2^32 - 1), and the
@@ -19,26 +19,25 @@
 namespace ivm {
 
 // word k of the split: (low 32 bits, high bits) of V_k; c_i = 0 outside [0, nc).
-// Src::quad(k) returns c_{4k .. 4k+3} (only called when 4k + 3 < nc);
-// Src::one(i) returns c_i.
+// Src::quad(k, c) fills c_{4k .. 4k+3} (only called when 4k + 3 < nc);
+// Src::one(i) returns c_i.  Coefficients are < 2^33 (255^2 n, n <= 2^17), so
+// V_k < 2^58 and hi_k < 2^26.
 template <typename Src>
 static __device__ __forceinline__ void carry_word(const Src &src, int nc, int k, unsigned &lo, unsigned &hi) {
   if (k < 0 || 4 * k >= nc) {
     lo = hi = 0u;
     return;
   }
-  unsigned c0, c1, c2, c3;
+  unsigned long long c[4];
   if (4 * k + 3 < nc) {
-    const int4 q = src.quad(k);
-    c0 = (unsigned)q.x, c1 = (unsigned)q.y, c2 = (unsigned)q.z, c3 = (unsigned)q.w;
+    src.quad(k, c);
   } else {
-    c0 = (unsigned)src.one(4 * k);
-    c1 = 4 * k + 1 < nc ? (unsigned)src.one(4 * k + 1) : 0u;
-    c2 = 4 * k + 2 < nc ? (unsigned)src.one(4 * k + 2) : 0u;
-    c3 = 0u;
+    c[0] = src.one(4 * k);
+    c[1] = 4 * k + 1 < nc ? src.one(4 * k + 1) : 0ull;
+    c[2] = 4 * k + 2 < nc ? src.one(4 * k + 2) : 0ull;
+    c[3] = 0ull;
   }
-  const unsigned long long v = (unsigned long long)c0 + ((unsigned long long)c1 << 8) +
-                               ((unsigned long long)c2 << 16) + ((unsigned long long)c3 << 24);
+  const unsigned long long v = c[0] + (c[1] << 8) + (c[2] << 16) + (c[3] << 24);
   lo = (unsigned)v;
   hi = (unsigned)(v >> 32);
 }
@@ -46,8 +45,11 @@ static __device__ __forceinline__ void carry_word(const Src &src, int nc, int k,
 // a plain [nc] int32 array (16-byte aligned)
 struct CoefLinear {
   const int32_t *c;
-  __device__ __forceinline__ int4 quad(int k) const { return reinterpret_cast<const int4 *>(c)[k]; }
-  __device__ __forceinline__ int one(int i) const { return c[i]; }
+  __device__ __forceinline__ void quad(int k, unsigned long long (&o)[4]) const {
+    const int4 q = reinterpret_cast<const int4 *>(c)[k];
+    o[0] = (unsigned)q.x, o[1] = (unsigned)q.y, o[2] = (unsigned)q.z, o[3] = (unsigned)q.w;
+  }
+  __device__ __forceinline__ unsigned long long one(int i) const { return (unsigned)c[i]; }
 };
 
 // per step: u (mod 2^32) and the generate / propagate bits of this lane's word.

@@ -66,6 +66,16 @@ int v4_table_entries(int m);
 int v4_tables(int m, int prec, const void *w2N, void *out);
 int v4_info(int prec, int m, LaunchInfo *li);
 int v4_launch(int prec, int m, const KParams &kp, int clusters, cudaStream_t s);
+// m = 2^17, 2^18: co-resident groups of m/8192 CTAs exchanging through L2 scratch
+struct Group5Args {
+  unsigned *ctr;   // [groups], zeroed before every launch
+  void *xch;       // [groups][C][4096] complex intervals
+  long long *coef;  // [groups][m]
+  unsigned *link;   // [groups][C][8]
+};
+int upload_w64_v5(const double *w64, const float *w32);
+int v5_info(int prec, int m, LaunchInfo *li);
+int v5_launch(int prec, int m, const KParams &kp, const Group5Args &ga, int groups, cudaStream_t s);
 int v3g_launch(int prec, int m, const KParams &kp, const GroupArgs &ga, int grid, cudaStream_t s);
 
 }  // namespace ivm

@@ -395,18 +395,19 @@ struct CertAcc {  // per-thread; reduced once per multiplication
   double rad = 0.0;
 };
 
-// coefficient i (global index) -> *dst (the snapped integer, or 0)
-template <typename T>
-__device__ __forceinline__ void certify_real(T lo, T hi, int i, int n, int32_t *dst, CertAcc &acc,
-                                             double *dump) {
+// coefficient i (global index) -> *dst (the snapped integer, or 0).  An int32
+// destination certifies only values that fit (n <= 32768 keeps 255^2 n < 2^31;
+// larger sizes use int64 destinations)
+template <typename T, typename D>
+__device__ __forceinline__ void certify_real(T lo, T hi, int i, int n, D *dst, CertAcc &acc, double *dump) {
   if (dump) reinterpret_cast<double4 *>(dump)[i] = make_double4((double)lo, (double)hi, 0.0, 0.0);
   if (i >= 2 * n - 1) return;
   const double l = (double)lo, h = (double)hi;
   const double cl = ceil(l);
-  const bool ok = cl == floor(h);
+  const bool ok = cl == floor(h) && (sizeof(D) == 8 || cl <= 2147483647.0);
   const double rad = __dmul_ru(__dadd_ru(h, -l), 0.5);
   acc.rad = (rad <= acc.rad) ? acc.rad : rad;  // NaN propagates (comparison false)
-  *dst = ok ? (int32_t)cl : 0;
+  *dst = ok ? (D)cl : (D)0;
   if (!ok) {
     acc.ok = 0;
     acc.bad = min(acc.bad, i);

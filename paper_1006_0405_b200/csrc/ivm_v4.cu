@@ -79,6 +79,11 @@ template <typename F, int M> static int v4_tables_impl(const F *w2N /* [2m][4] *
       memcpy(out + 2L * (X::TH(c) + 2 * q), w2N + 4L * e, 4 * sizeof(F));  // full interval
     }
   }
+  for (int j = 0; j < C; j++) {  // w_C^{-j} and z^{-4096 j}
+    const long e1 = ((-(long)j * (N2 / C)) % N2 + N2) % N2, e2 = ((-(long)j * 4096) % N2 + N2) % N2;
+    memcpy(out + 2L * (X::S2 + 2 * j), w2N + 4L * e1, 4 * sizeof(F));
+    memcpy(out + 2L * (X::FO + 2 * j), w2N + 4L * e2, 4 * sizeof(F));
+  }
   return ok ? X::TOTAL : -4;
 }
 
@@ -89,15 +94,24 @@ template <typename F, int M> static int v4_tables_impl(const F *w2N /* [2m][4] *
     case 16: return FN<16>(__VA_ARGS__); \
     default: return -4;                \
   }
+#define IVM_V45_DISPATCH(FN, ...)      \
+  switch (m) {                         \
+    case 14: return FN<14>(__VA_ARGS__); \
+    case 15: return FN<15>(__VA_ARGS__); \
+    case 16: return FN<16>(__VA_ARGS__); \
+    case 17: return FN<17>(__VA_ARGS__); \
+    case 18: return FN<18>(__VA_ARGS__); \
+    default: return -4;                \
+  }
 
 template <int M> static int v4_entries_m() { return v4::G4<M>::TOTAL; }
-int v4_table_entries(int m) { IVM_V4_DISPATCH(v4_entries_m) }
+int v4_table_entries(int m) { IVM_V45_DISPATCH(v4_entries_m) }
 
 template <int M> static int v4_tables_m(int prec, const void *w2N, void *out) {
   return prec == 0 ? v4_tables_impl<double, M>((const double *)w2N, (double *)out)
                    : v4_tables_impl<float, M>((const float *)w2N, (float *)out);
 }
-int v4_tables(int m, int prec, const void *w2N, void *out) { IVM_V4_DISPATCH(v4_tables_m, prec, w2N, out) }
+int v4_tables(int m, int prec, const void *w2N, void *out) { IVM_V45_DISPATCH(v4_tables_m, prec, w2N, out) }
 
 template <typename T, int M> static int v4_info_impl(LaunchInfo *li) {
   using CF = v4::Cfg4<T, M>;

@@ -26,7 +26,7 @@ namespace v4 {
 using namespace v3;
 
 template <int M> struct G4 {
-  static_assert(M >= 14 && M <= 16, "cluster sizes 2, 4, 8");
+  static_assert(M >= 14 && M <= 18, "C = 2 .. 32 CTAs");
   static constexpr int C = 1 << (M - 13);
   static constexpr int B = 4096 / C;  // rows of the last inverse pass per CTA
   static constexpr int LGB = 12 - (M - 13);
@@ -37,19 +37,25 @@ template <int M> struct G4 {
   //   INV:    local inverse passes 1..3: [7][8], [7][64], [7][512] (shared)
   //   XINV(c): role c, last inverse pass, [C][B] (rows c B .. c B + B - 1), folded untwist
   //   TH(c):  role c, theta_q (q < C) as full intervals (2 entries each)
+  //   S2:     w_C^{-j}, j < C (full intervals; v5's two-stage last inverse pass)
+  //   FO:     conj(w_{4C}^r) = z^{-4096 r}, r < C (full intervals; v5's emit)
   __host__ __device__ static constexpr int FWD(int c) { return c * 4096; }
   __host__ __device__ static constexpr int FP(int p) { return p == 1 ? 0 : (p == 2 ? 7 : (p == 3 ? 63 : 512)); }
   static constexpr int INV = C * 4096;
   static constexpr int INV1 = 0, INV2 = 56, INV3 = 504, INV_ENT = 4088;
   __host__ __device__ static constexpr int XINV(int c) { return INV + 4096 + c * 4096; }
   __host__ __device__ static constexpr int TH(int c) { return INV + 4096 + C * 4096 + 2 * C * c; }
-  static constexpr int TOTAL = INV + 4096 + C * 4096 + 2 * C * C;
+  static constexpr int S2 = INV + 4096 + C * 4096 + 2 * C * C;
+  static constexpr int FO = S2 + 2 * C;
+  static constexpr int TOTAL = FO + 2 * C;
   // shared-memory twiddle area (entries)
   static constexpr int S_SWAP = 0;          // 4096: forward-last -> inverse pass 3 -> last inverse pass
   static constexpr int S_MF = 4096;         // forward passes 1..3 (511 entries + 1 pad)
   static constexpr int S_MI = 4096 + 512;   // inverse passes 1, 2 (504 entries)
   static constexpr int S_TH = 4096 + 1016;  // theta (2C entries)
-  static constexpr int S_ENT = S_TH + 2 * C;
+  static constexpr int S_S2 = S_TH + 2 * C;  // v5 only
+  static constexpr int S_FO = S_S2 + 2 * C;  // v5 only
+  static constexpr int S_ENT = S_TH + 2 * C;  // v4 (v5: S_FO + 2 C)
   static constexpr int FLAST = 3584, MF_ENT = 512, MI_ENT = 504;
 };
 
@@ -138,8 +144,11 @@ template <int M> struct CoefCluster {
     const int idx = (h * X::C + r) * X::B + (k0 - (p << X::LGB));
     return dsm_map_addr(base + 4u * (unsigned)idx, (unsigned)p);
   }
-  __device__ __forceinline__ int4 quad(int k) const { return dsm_ld_i4(addr(4 * k)); }
-  __device__ __forceinline__ int one(int i) const { return dsm_ld_i32(addr(i)); }
+  __device__ __forceinline__ void quad(int k, unsigned long long (&o)[4]) const {
+    const int4 q = dsm_ld_i4(addr(4 * k));
+    o[0] = (unsigned)q.x, o[1] = (unsigned)q.y, o[2] = (unsigned)q.z, o[3] = (unsigned)q.w;
+  }
+  __device__ __forceinline__ unsigned long long one(int i) const { return (unsigned)dsm_ld_i32(addr(i)); }
 };
 
 // first (cross-CTA) forward pass from the digits: row `crank` of level 2C,
@@ -391,7 +400,8 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
     }
     if (kp.coeffs) {
       int64_t *co = kp.coeffs + (size_t)pair * nc;
-      for (int i = 4 * kb + (int)threadIdx.x; i < min(4 * ke, nc); i += blockDim.x) co[i] = ok ? src.one(i) : 0;
+      for (int i = 4 * kb + (int)threadIdx.x; i < min(4 * ke, nc); i += blockDim.x)
+        co[i] = ok ? (int64_t)src.one(i) : 0;
     }
     if (crank == 0 && threadIdx.x == 0) {
       kp.cert[pair] = ok ? 1 : 0;

@@ -1,0 +1,76 @@
+// ivm_v5.cu -- translation unit of the group kernel for m = 2^17, 2^18
+// (ivm_v5.cuh): launch info and the cooperative launch.  Its twiddle tables are
+// the v4 layout (v4_tables, ivm_v4.cu).
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include "ivm_interval.cuh"
+#include "ivm_internal.h"
+#include "ivm_carry.cuh"
+#include "ivm_v3.cuh"
+#include "ivm_v4.cuh"
+#include "ivm_v5.cuh"
+#include "ivm_twc_host.h"
+
+namespace ivm {
+
+int upload_w64_v5(const double *w64, const float *w32) {  // this TU's DFT-internal constants
+  v3::TwC<double> d[17];
+  v3::TwC<float> f[17];
+  for (int j = 0; j <= 16; j++) {
+    double o[2];
+    float of[2];
+    if (!compact(w64 + 4 * j, o) || !compact(w32 + 4 * j, of)) return -4;
+    d[j] = v3::TwC<double>{o[0], o[1]};
+    f[j] = v3::TwC<float>{of[0], of[1]};
+  }
+  if (cudaMemcpyToSymbol(v3::c_w64_f64, d, sizeof(d)) != cudaSuccess) return -1;
+  if (cudaMemcpyToSymbol(v3::c_w64_f32, f, sizeof(f)) != cudaSuccess) return -1;
+  return 0;
+}
+
+template <typename T, int M> static int v5_info_impl(LaunchInfo *li) {
+  using CF = v5::Cfg5<T, M>;
+  auto k = v5::ivm_v5_kernel<T, M>;
+  li->threads = CF::THREADS;
+  li->smem = CF::SMEM;
+  li->a_smem = false;
+  li->a_bytes_per_cta = CF::A_BYTES;
+  li->cluster = v4::G4<M>::C;
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM) != cudaSuccess) return -1;
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, CF::THREADS, CF::SMEM) != cudaSuccess) return -1;
+  li->blocks_per_sm = nb;
+  li->max_clusters = 0;
+  return 0;
+}
+#define IVM_V5_DISPATCH(FN, ...)         \
+  switch (m) {                           \
+    case 17: return FN<17>(__VA_ARGS__); \
+    case 18: return FN<18>(__VA_ARGS__); \
+    default: return -4;                  \
+  }
+template <int M> static int v5_info_m(int prec, LaunchInfo *li) {
+  return prec == 0 ? v5_info_impl<double, M>(li) : v5_info_impl<float, M>(li);
+}
+int v5_info(int prec, int m, LaunchInfo *li) { IVM_V5_DISPATCH(v5_info_m, prec, li) }
+
+template <typename T, int M> static int v5_go(const KParams &kp, const Group5Args &ga, int groups, cudaStream_t s) {
+  using CF = v5::Cfg5<T, M>;
+  KParams k2 = kp;
+  v5::Group5 g{ga.ctr, ga.xch, ga.coef, ga.link};
+  void *args[] = {(void *)&k2, (void *)&g};
+  return cudaLaunchCooperativeKernel((const void *)v5::ivm_v5_kernel<T, M>, dim3(groups * v4::G4<M>::C),
+                                     dim3(CF::THREADS), args, CF::SMEM, s) == cudaSuccess
+             ? 0
+             : -1;
+}
+template <int M> static int v5_launch_m(int prec, const KParams &kp, const Group5Args &ga, int groups, cudaStream_t s) {
+  return prec == 0 ? v5_go<double, M>(kp, ga, groups, s) : v5_go<float, M>(kp, ga, groups, s);
+}
+int v5_launch(int prec, int m, const KParams &kp, const Group5Args &ga, int groups, cudaStream_t s) {
+  IVM_V5_DISPATCH(v5_launch_m, prec, kp, ga, groups, s)
+}
+
+}  // namespace ivm

@@ -1,0 +1,316 @@
+// ivm_v5.cuh -- group kernel for m = 2^17, 2^18 (C = 16, 32 CTAs per
+// multiplication; included by ivm_v5.cu).
+//
+// The same row split and local m = 8192 schedule as the cluster kernel
+// (ivm_v4.cuh), for groups too large for a thread-block cluster: the C CTAs of
+// a group are co-resident (cooperative launch) and exchange through L2-resident
+// global scratch with group barriers (global atomics) instead of DSMEM.
+//   * after the local inverse passes 0..3 every CTA writes its column of the
+//     4096 inverse rows to scratch; barrier;
+//   * CTA c gathers rows [c B, c B + B) of all C columns and runs the last
+//     inverse pass (radix C, untwist folded into the input twiddles) as two
+//     shared-memory stages, C = 8 C2:
+//       out_{r1 + 8 r2} = sum_b w_{C2}^{-b r2} [ w_C^{-b r1} sum_a w_8^{-a r1} y_{C2 a + b} ],
+//     then scales, certifies and snaps c_k, c_{k+m/2} (k = k0 + 4096 r) into a
+//     global int32 coefficient array; barrier;
+//   * carry over contiguous word segments, group-level ballot adder through
+//     global link words; barrier.
+#pragma once
+
+namespace ivm {
+namespace v5 {
+
+using namespace v3;
+using namespace v4;
+
+struct Group5 {
+  unsigned *ctr;   // [groups] barrier counters (zeroed by the host before the launch)
+  void *xch;       // [groups][C][4096] CI<T> column exchange
+  long long *coef;  // [groups][m] coefficients (up to 255^2 n > 2^31)
+  unsigned *link;  // [groups][C][8] per-CTA certificate / carry words
+};
+
+// coefficients written by other SMs: read through L2 only (no stale L1 lines)
+struct CoefGlobalCG {
+  const long long *c;
+  __device__ __forceinline__ void quad(int k, unsigned long long (&o)[4]) const {
+    const longlong2 a = __ldcg(reinterpret_cast<const longlong2 *>(c) + 2 * k);
+    const longlong2 b = __ldcg(reinterpret_cast<const longlong2 *>(c) + 2 * k + 1);
+    o[0] = (unsigned long long)a.x, o[1] = (unsigned long long)a.y, o[2] = (unsigned long long)b.x,
+    o[3] = (unsigned long long)b.y;
+  }
+  __device__ __forceinline__ unsigned long long one(int i) const { return (unsigned long long)__ldcg(c + i); }
+};
+
+template <typename T> __device__ __forceinline__ CI<T> ldcg_ci(const CI<T> *p) {
+  if constexpr (sizeof(T) == 8) {
+    const double2 a = __ldcg(reinterpret_cast<const double2 *>(p)), b = __ldcg(reinterpret_cast<const double2 *>(p) + 1);
+    return CI<T>{a.x, a.y, b.x, b.y};
+  } else {
+    const float4 a = __ldcg(reinterpret_cast<const float4 *>(p));
+    return CI<T>{a.x, a.y, a.z, a.w};
+  }
+}
+
+__device__ __forceinline__ void gsync(unsigned *ctr, unsigned C, unsigned &gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned target = (gen + 1u) * C;
+    atomicAdd(ctr, 1u);
+    while (*(volatile unsigned *)ctr < target) {
+    }
+    __threadfence();
+  }
+  gen++;
+  __syncthreads();
+}
+
+template <typename T, int M> struct Cfg5 {
+  using GL = G3<13, 8>;
+  static constexpr int THREADS = 512;
+  static constexpr size_t E = sizeof(typename V2t<T>::t);
+  static constexpr size_t STATE_BYTES = 2 * E * (size_t)GL::CAP;
+  static constexpr int S_ENT = G4<M>::S_FO + 2 * G4<M>::C;
+  static constexpr size_t TW_BYTES = sizeof(TwC<T>) * (size_t)S_ENT;
+  static constexpr size_t SMEM = STATE_BYTES + TW_BYTES;
+  static constexpr size_t A_BYTES = 2 * E * 4096;
+  static_assert(SMEM <= 227 * 1024, "shared memory");
+};
+
+// c = 2 Re / m, 2 Im / m of t = w o (w: full interval), certified into d0, d1
+template <typename T, int M>
+__device__ __forceinline__ void emit_tab(const CI<T> &o, const CI<T> &w, int k, int n, long long *d0, long long *d1,
+                                         CertAcc &acc, double *dump) {
+  constexpr int N = 1 << M;
+  const CI<T> v = cmul(w, o);
+  const T s = T(2) / T(N);
+  certify_real(DR<T>::mul_rd(v.rl, s), DR<T>::mul_ru(v.rh, s), k, n, d0, acc, dump);
+  certify_real(DR<T>::mul_rd(v.il, s), DR<T>::mul_ru(v.ih, s), k + N / 2, n, d1, acc, dump);
+}
+
+template <typename T, int M>
+__global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
+  using X = G4<M>;
+  using GL = G3<13, 8>;
+  using CF = Cfg5<T, M>;
+  using V = typename V2t<T>::t;
+  constexpr int C = X::C, B = X::B, C2 = C / 8, R = 8, NL = 8192, N = 1 << M;
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ Cert3 cs;
+  __shared__ CarrySeg seg;
+  __shared__ __align__(8) unsigned long long tbar;
+  Buf<T> st{reinterpret_cast<V *>(smem), reinterpret_cast<V *>(smem) + GL::CAP};
+  TwC<T> *twb = reinterpret_cast<TwC<T> *>(smem + CF::STATE_BYTES);
+  const CI<T> *theta = reinterpret_cast<const CI<T> *>(twb + X::S_TH);
+  const CI<T> *s2tw = reinterpret_cast<const CI<T> *>(twb + X::S_S2);
+  const CI<T> *fold = reinterpret_cast<const CI<T> *>(twb + X::S_FO);
+  const unsigned crank = blockIdx.x % C;
+  const int gi = (int)(blockIdx.x / C), ngr = (int)(gridDim.x / C);
+  unsigned *ctr = g.ctr + gi;
+  CI<T> *xch = reinterpret_cast<CI<T> *>(g.xch) + (size_t)gi * C * 4096;
+  long long *gcoef = g.coef + (size_t)gi * N;
+  unsigned *link = g.link + (size_t)gi * C * 8;
+  unsigned gen = 0;
+  const TwC<T> *tw = reinterpret_cast<const TwC<T> *>(kp.tw);
+  Buf<T> A{reinterpret_cast<V *>(kp.ascratch) + (size_t)blockIdx.x * NL, nullptr};
+  A.im = A.re + NL / 2;
+  const int n = kp.n, nc = 2 * n - 1, nout = 2 * n;
+  constexpr int RSI1 = GL::iRS(1), SWI1 = GL::iSW(1);
+  constexpr unsigned EB = sizeof(TwC<T>);
+
+  if (threadIdx.x == 0) mbar_init(&tbar);
+  __syncthreads();
+  if (threadIdx.x == 0 && gi < kp.batch) {
+    mbar_expect(&tbar, EB * (X::FLAST + X::MF_ENT + X::MI_ENT + 6 * C));
+    bulk_copy(twb + X::S_SWAP, tw + X::FWD(crank) + X::FP(4), EB * X::FLAST, &tbar);
+    bulk_copy(twb + X::S_MF, tw + X::FWD(crank), EB * X::MF_ENT, &tbar);
+    bulk_copy(twb + X::S_MI, tw + X::INV, EB * X::MI_ENT, &tbar);
+    bulk_copy(twb + X::S_TH, tw + X::TH(crank), EB * 2 * C, &tbar);
+    bulk_copy(twb + X::S_S2, tw + X::S2, EB * 4 * C, &tbar);  // S2 and FO are adjacent
+  }
+  if (gi < kp.batch) mbar_wait(&tbar, 0);
+
+  int it = 0;
+  for (int pair = gi; pair < kp.batch; pair += ngr, it++) {
+    const unsigned par = (unsigned)it & 1u;
+    if (pair + ngr < kp.batch) {  // L2 prefetch of the next pair's digits (this CTA's slice)
+      const int nxt = pair + ngr, sl = (n + C - 1) / C;
+      for (int off = (int)crank * sl + (int)threadIdx.x * 128; off < min(n, ((int)crank + 1) * sl);
+           off += (int)blockDim.x * 128) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(kp.a + (size_t)nxt * n + off));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(kp.b + (size_t)nxt * n + off));
+      }
+    }
+#pragma unroll 1
+    for (int op = 0; op < 2; op++) {
+      cross_fwd<T, M>((op == 0 ? kp.a : kp.b) + (size_t)pair * n, n, st, theta, crank);
+      if (op == 1 && threadIdx.x == 0) {
+        cs.ok = 1;
+        cs.first_bad = 0x7fffffff;
+        cs.maxrad = 0ull;
+      }
+      __syncthreads();
+#pragma unroll 1
+      for (int i = 0; i < 4; i++) {
+        const PassRT pp = pick_fwd4<M>(i);
+        CI<T> v[R];
+        int k0, nu;
+        if (op == 0 && i == 3) mbar_wait(&tbar, par);
+        fwdR<T, R>(st, twb, pp, v, k0, nu);
+        if (i < 3) {
+          __syncthreads();
+#pragma unroll
+          for (int r = 0; r < R; r++) {
+            if (2 * r < R) st.st(sidx(k0 + pp.L * r, nu, pp.RSo, pp.SWo), v[r]);
+            else st.st(sidx(R * pp.L - 1 - k0 - pp.L * r, nu, pp.RSo, pp.SWo), cconj(v[r]));
+          }
+        } else if (op == 0) {
+#pragma unroll
+          for (int r = 0; r < R; r++) A.st(r * (pp.L >> 1) + k0, v[r]);
+        } else {
+          CI<T> an = A.ld(k0);
+#pragma unroll
+          for (int r = 0; r < R; r++) {
+            const CI<T> a = an;
+            if (r + 1 < R) an = A.ld((r + 1) * (pp.L >> 1) + k0);
+            v[r] = cmul(a, v[r]);
+          }
+          cdft<T, R, true>(v);
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            mbar_expect(&tbar, EB * X::FLAST);
+            bulk_copy(twb + X::S_SWAP, tw + X::INV + X::INV3, EB * X::FLAST, &tbar);
+          }
+#pragma unroll
+          for (int r = 0; r < R; r++) st.st(sidx(r, k0, RSI1, SWI1), v[r]);
+        }
+        __syncthreads();
+      }
+    }
+#pragma unroll 1
+    for (int i = 0; i < 3; i++) {
+      const PassRT pp = pick_inv4<M>(i);
+      CI<T> v[R];
+      int k0, nu;
+      if (i == 2) mbar_wait(&tbar, par ^ 1u);
+      invR<T, R, false>(st, twb, pp, v, k0, nu);
+      if (i < 2) {
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < R; r++) st.st(sidx(k0 + pp.L * r, nu, pp.RSo, pp.SWo), v[r]);
+        __syncthreads();
+      } else {  // last local pass: the column goes to the group's exchange scratch (row k0 + L r)
+#pragma unroll
+        for (int r = 0; r < R; r++) xch[(size_t)crank * 4096 + k0 + pp.L * r] = v[r];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // last inverse pass table (this role's rows)
+      mbar_expect(&tbar, EB * 4096);
+      bulk_copy(twb + X::S_SWAP, tw + X::XINV(crank), EB * 4096, &tbar);
+    }
+    gsync(ctr, C, gen);  // (1) all columns written
+    mbar_wait(&tbar, par);
+    // gather + input twiddles: y_q(kl) -> state[q B + kl]
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      const int idx = (int)threadIdx.x + 512 * j, q = idx / B, kl = idx % B;
+      const int src = (2 * q < C) ? 2 * q : 2 * C - 1 - 2 * q;
+      CI<T> z = ldcg_ci(xch + (size_t)src * 4096 + (int)crank * B + kl);
+      const TwC<T> w = twb[X::S_SWAP + q * B + kl];
+      z = (2 * q < C) ? rtmul<T, true, true>(w, z) : rtmul<T, false, true>(w, cconj(z));
+      st.st(idx, z);
+    }
+    __syncthreads();
+    {  // stage 1: task (b, kl), DFT8 over a, times w_C^{-b r1}
+      const int b = (int)threadIdx.x / B, kl = (int)threadIdx.x % B;
+      CI<T> v[8];
+#pragma unroll
+      for (int a = 0; a < 8; a++) v[a] = st.ld((C2 * a + b) * B + kl);
+      cdft<T, 8, true>(v);
+#pragma unroll
+      for (int r1 = 1; r1 < 8; r1++) v[r1] = cmul(s2tw[b * r1], v[r1]);
+      __syncthreads();
+#pragma unroll
+      for (int r1 = 0; r1 < 8; r1++) st.st((r1 * C2 + b) * B + kl, v[r1]);
+      __syncthreads();
+    }
+    CertAcc acc;
+    {  // stage 2: task (r1, kl), DFT_C2 over b, untwist remainder, emit
+      double *dump = diag_dump(kp, pair, N);
+      constexpr int TASKS = 8 * B / 512;
+#pragma unroll
+      for (int g2 = 0; g2 < TASKS; g2++) {
+        const int task = (int)threadIdx.x + 512 * g2, r1 = task / B, kl = task % B;
+        const int k0 = (int)crank * B + kl;
+        CI<T> v[C2];
+#pragma unroll
+        for (int b = 0; b < C2; b++) v[b] = st.ld((r1 * C2 + b) * B + kl);
+        cdft<T, C2, true>(v);
+#pragma unroll
+        for (int r2 = 0; r2 < C2; r2++) {
+          const int r = r1 + 8 * r2, k = k0 + 4096 * r;
+          emit_tab<T, M>(v[r2], fold[r], k, n, gcoef + k, gcoef + k + N / 2, acc, dump);
+        }
+      }
+    }
+    cert_flush(acc, cs);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      link[crank * 8 + 0] = (unsigned)cs.ok;
+      link[crank * 8 + 1] = (unsigned)cs.first_bad;
+      link[crank * 8 + 2] = (unsigned)(cs.maxrad & 0xffffffffu);
+      link[crank * 8 + 3] = (unsigned)(cs.maxrad >> 32);
+      if (pair + ngr < kp.batch) {  // next pair's forward-last table
+        mbar_expect(&tbar, EB * X::FLAST);
+        bulk_copy(twb + X::S_SWAP, tw + X::FWD(crank) + X::FP(4), EB * X::FLAST, &tbar);
+      }
+    }
+    gsync(ctr, C, gen);  // (2) coefficients and certificates of every CTA visible
+    int ok = 1, bad = 0x7fffffff;
+    unsigned long long rad = 0ull;
+    for (int p = 0; p < C; p++) {
+      const volatile unsigned *lp = link + p * 8;
+      ok &= (int)lp[0];
+      bad = min(bad, (int)lp[1]);
+      const unsigned long long rp = (unsigned long long)lp[2] | ((unsigned long long)lp[3] << 32);
+      rad = rp > rad ? rp : rad;
+    }
+    const int words = (nout + 3) / 4, wc = (words + C - 1) / C;
+    const int kb = min((int)crank * wc, words), ke = min(kb + wc, words);
+    uint8_t *out = kp.prod + (size_t)pair * nout;
+    const CoefGlobalCG src{gcoef};
+    unsigned gn = 0u, ap = 1u;
+    if (ok) carry_seg_scan(src, nc, kb, ke, seg, gn, ap);
+    if (threadIdx.x == 0) {
+      link[crank * 8 + 4] = gn;
+      link[crank * 8 + 5] = ap;
+    }
+    gsync(ctr, C, gen);  // (3) per-CTA generate / all-propagate visible
+    if (ok) {
+      // carry into this CTA: scan of (generate, all-propagate) over the CTAs below
+      unsigned cin = 0u;
+      for (unsigned p = 0; p < crank; p++) {
+        const volatile unsigned *lp = link + p * 8;
+        cin = lp[4] | (lp[5] & cin);
+      }
+      carry_seg_emit(src, nc, nout, kb, ke, seg, cin, out);
+    } else {
+      for (int i = 4 * kb + (int)threadIdx.x; i < min(4 * ke, nout); i += blockDim.x) out[i] = 0;
+    }
+    if (kp.coeffs) {
+      int64_t *co = kp.coeffs + (size_t)pair * nc;
+      for (int i = 4 * kb + (int)threadIdx.x; i < min(4 * ke, nc); i += blockDim.x)
+        co[i] = ok ? (int64_t)src.one(i) : 0;
+    }
+    if (crank == 0 && threadIdx.x == 0) {
+      kp.cert[pair] = ok ? 1 : 0;
+      if (kp.max_radius) kp.max_radius[pair] = __longlong_as_double((long long)rad);
+      if (kp.first_bad) kp.first_bad[pair] = ok ? -1 : bad;
+    }
+  }
+}
+
+}  // namespace v5
+}  // namespace ivm
