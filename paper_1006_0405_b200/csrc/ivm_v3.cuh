@@ -395,16 +395,17 @@ struct CertAcc {  // per-thread; reduced once per multiplication
   double rad = 0.0;
 };
 
-// coefficient i (global index) -> *dst (the snapped integer, or 0).  An int32
-// destination certifies only values that fit (n <= 32768 keeps 255^2 n < 2^31;
-// larger sizes use int64 destinations)
+// coefficient i (global index) -> *dst (the snapped integer, or 0).  int32
+// destinations are used only for n <= 32768 (m <= 2^16), where every certified
+// coefficient is an exact convolution value <= 255^2 n < 2^31; m = 2^17, 2^18
+// use int64 destinations (v5)
 template <typename T, typename D>
 __device__ __forceinline__ void certify_real(T lo, T hi, int i, int n, D *dst, CertAcc &acc, double *dump) {
   if (dump) reinterpret_cast<double4 *>(dump)[i] = make_double4((double)lo, (double)hi, 0.0, 0.0);
   if (i >= 2 * n - 1) return;
   const double l = (double)lo, h = (double)hi;
   const double cl = ceil(l);
-  const bool ok = cl == floor(h) && (sizeof(D) == 8 || cl <= 2147483647.0);
+  const bool ok = cl == floor(h);
   const double rad = __dmul_ru(__dadd_ru(h, -l), 0.5);
   acc.rad = (rad <= acc.rad) ? acc.rad : rad;  // NaN propagates (comparison false)
   *dst = ok ? (D)cl : (D)0;
