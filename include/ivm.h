@@ -123,6 +123,33 @@ int ivm_multiply_batched_host(ivm_ctx_t ctx, const uint8_t *a, const uint8_t *b,
                               size_t batch, uint8_t *prod, uint8_t *certified, int prec,
                               void *cuda_stream);
 
+/* Exact long multiplication on the device (the paper's
+ * guaranteed-correct comparator): prod[p] = a[p] * b[p] exactly, no FFT
+ * and no rounding.  a, b: device [batch][n] digits (least significant first);
+ * prod: device [batch][2n].  The sums s_k = sum_{i+j=k} a_i b_j are formed
+ * exactly (byte dot products, 64-bit accumulation) in context-owned device
+ * scratch (<= 256 MiB per launch, pairs chunked), then carried.
+ * Requires n <= 2^18 (IVM_EUNSUPPORTED otherwise).  Asynchronous on
+ * `cuda_stream`. */
+int ivm_long_multiply_batched(ivm_ctx_t ctx, const uint8_t *a, const uint8_t *b, size_t n,
+                              size_t batch, uint8_t *prod, void *cuda_stream);
+
+/* Exact products with the paper's escalation (when an error is
+ * detected, "increase the precision being used or ... use a different
+ * algorithm").  policy 0 (the paper's order): the fp32 interval FFT when
+ * n <= 32, else the fp64 one; the fp64 interval FFT for the pairs fp32 did not
+ * certify; exact long multiplication for the pairs fp64 did not certify (and
+ * for n > ivm_max_digits(IVM_F64)).  policy 1 (fastest exact): long
+ * multiplication when the FFT length is below 1024 (where it is faster on
+ * B200), else fp64 then long multiplication.
+ * prod: device [batch][2n], always the exact product.  method: device
+ * [batch] or NULL; receives 1 (fp32 interval), 2 (fp64 interval) or 3 (long
+ * multiplication) per pair.  Synchronises `cuda_stream` (the uncertified
+ * counts size the later tiers).  Uses context-owned device scratch.
+ * IVM_EINVAL for a bad policy. */
+int ivm_multiply_exact(ivm_ctx_t ctx, const uint8_t *a, const uint8_t *b, size_t n, size_t batch,
+                       uint8_t *prod, uint8_t *method, int policy, void *cuda_stream);
+
 /* Seeded synthetic digits on the device (the counter-based SplitMix64
  * generator of SURVEY.md §8(d.2); same bits as
  * paper_1006_0405_b200/inputs.py).  kind: 0 uniform, 1 all-255, 2 sparse

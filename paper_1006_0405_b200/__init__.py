@@ -21,7 +21,8 @@ LIB_PATH = os.path.join(_HERE, "libivm.so")
 EXPORTS = ["ivm_version", "ivm_strerror", "ivm_max_digits", "ivm_fft_length", "ivm_create",
            "ivm_destroy", "ivm_reserve", "ivm_multiply", "ivm_multiply_batched",
            "ivm_multiply_batched_diag", "ivm_multiply_batched_host", "ivm_generate_digits",
-           "ivm_peak_probe", "ivm_last_launch_count", "ivm_twiddle_table"]
+           "ivm_peak_probe", "ivm_last_launch_count", "ivm_twiddle_table", "ivm_long_multiply_batched",
+           "ivm_multiply_exact"]
 
 
 class IvmError(RuntimeError):
@@ -61,6 +62,8 @@ def lib():
         L.ivm_peak_probe.argtypes = [P, I, I, P, ctypes.POINTER(U64), P]
         L.ivm_last_launch_count.argtypes = [P]
         L.ivm_twiddle_table.argtypes = [I, I, P]
+        L.ivm_long_multiply_batched.argtypes = [P, P, P, S, S, P, P]
+        L.ivm_multiply_exact.argtypes = [P, P, P, S, S, P, P, I, P]
         _lib = L
     return _lib
 
@@ -167,6 +170,31 @@ class Context:
                "ivm_multiply_batched_diag")
         return {"prod": out, "cert": cert, "max_radius": rad, "first_bad": bad, "coeffs": co,
                 "intervals": iv, "m": m}
+
+    def long_multiply(self, a, b, out=None, stream=None):
+        """Exact long multiplication on the device: [B][2n] u8."""
+        import torch
+        B, n = a.shape
+        if out is None:
+            out = torch.empty((B, 2 * n), dtype=torch.uint8, device=a.device)
+        _check(lib().ivm_long_multiply_batched(self._h, _ptr(a), _ptr(b), n, B, _ptr(out), _stream(stream)),
+               "ivm_long_multiply_batched")
+        return out
+
+    def multiply_exact(self, a, b, out=None, method=None, policy: int = 0, stream=None):
+        """Exact products with the fp32 -> fp64 -> long-multiplication
+        escalation (policy 1: long multiplication directly below
+        m = 1024); returns (products [B][2n] u8, method [B] u8:
+        1 fp32 interval, 2 fp64 interval, 3 long multiplication)."""
+        import torch
+        B, n = a.shape
+        if out is None:
+            out = torch.empty((B, 2 * n), dtype=torch.uint8, device=a.device)
+        if method is None:
+            method = torch.empty((B,), dtype=torch.uint8, device=a.device)
+        _check(lib().ivm_multiply_exact(self._h, _ptr(a), _ptr(b), n, B, _ptr(out), _ptr(method), policy,
+                                        _stream(stream)), "ivm_multiply_exact")
+        return out, method
 
     def multiply_host(self, a, b, prec: int = F64, out=None, cert=None, stream=None):
         """End-to-end path: host (pinned) uint8 tensors in, host tensors out."""

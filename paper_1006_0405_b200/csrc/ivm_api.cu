@@ -38,6 +38,8 @@ struct ivm_ctx {
   int last_launches = 0;
   void *gscratch = nullptr;  // large-m group scratch
   size_t gscratch_bytes = 0;
+  void *lscratch = nullptr;  // long multiplication sums / escalation buffers
+  size_t lscratch_bytes = 0;
   // host API pipeline: copy-in / copy-out streams and per-chunk events
   cudaStream_t s_in = nullptr, s_out = nullptr;
   std::vector<cudaEvent_t> ev;
@@ -137,6 +139,7 @@ int ivm_destroy(ivm_ctx_t c) {
   cudaFree(c->slot);
   cudaFree(c->stage);
   cudaFree(c->gscratch);
+  cudaFree(c->lscratch);
   if (c->s_in) cudaStreamDestroy(c->s_in);
   if (c->s_out) cudaStreamDestroy(c->s_out);
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
@@ -563,6 +566,131 @@ int ivm_multiply_batched_host(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, s
   }
   // `stream` completes after the last copy-out
   if (cudaStreamWaitEvent(s, c->ev[3 * (nchunks - 1) + 2], 0) != cudaSuccess) return cuda_fail(c);
+  c->last_launches = launches;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_fail(c);
+  return IVM_OK;
+}
+
+static int ensure_lscratch(ivm_ctx_t c, size_t bytes) {
+  if (bytes <= c->lscratch_bytes) return IVM_OK;
+  cudaFree(c->lscratch);
+  c->lscratch = nullptr;
+  c->lscratch_bytes = 0;
+  if (cudaMalloc(&c->lscratch, bytes) != cudaSuccess) return IVM_ENOMEM;
+  c->lscratch_bytes = bytes;
+  return IVM_OK;
+}
+
+static const size_t kLongMaxDigits = (size_t)1 << 18;  // sums < 255^2 n < 2^34 (word carry bound)
+static const size_t kLongChunkBytes = (size_t)256 << 20;
+
+static size_t long_chunk(size_t n, size_t batch) {  // pairs per launch (int64 sums <= 256 MiB)
+  size_t chunk = kLongChunkBytes / ((2 * n - 1) * 8);
+  if (chunk < 1) chunk = 1;
+  return chunk > batch ? batch : chunk;
+}
+
+// exact products of `batch` pairs; the int64 sums go to the long-multiplication
+// scratch at offset `off`, which the caller has sized for long_chunk(n, batch) pairs
+static int long_run(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, size_t n, size_t batch, uint8_t *prod,
+                    cudaStream_t s, size_t off, int *launches) {
+  const size_t nc = 2 * n - 1, chunk = long_chunk(n, batch);
+  long long *coef = (long long *)((char *)c->lscratch + off);
+  for (size_t p0 = 0; p0 < batch; p0 += chunk) {
+    const size_t pb = batch - p0 < chunk ? batch - p0 : chunk;
+    if (ivm::long_launch(a + p0 * n, b + p0 * n, (int)n, (int)pb, coef, prod + p0 * 2 * n, s) != 0)
+      return cuda_fail(c);
+    *launches += 2 + (int)((pb - 1) / 65535);
+  }
+  return IVM_OK;
+}
+
+int ivm_long_multiply_batched(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, size_t n, size_t batch,
+                              uint8_t *prod, void *stream) {
+  if (!c || !a || !b || !prod || n == 0 || batch == 0) return IVM_EINVAL;
+  if (n > kLongMaxDigits || batch > (size_t)0x7fffffff) return IVM_EUNSUPPORTED;
+  if (c->sticky) return c->sticky;
+  if (cudaSetDevice(c->device) != cudaSuccess) return cuda_fail(c);
+  int r = ensure_lscratch(c, long_chunk(n, batch) * (2 * n - 1) * 8);
+  if (r) return r;
+  int launches = 0;
+  r = long_run(c, a, b, n, batch, prod, (cudaStream_t)stream, 0, &launches);
+  c->last_launches = launches;
+  return r;
+}
+
+int ivm_multiply_exact(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, size_t n, size_t batch, uint8_t *prod,
+                       uint8_t *method, int policy, void *stream) {
+  if (!c || !a || !b || !prod || n == 0 || batch == 0 || (policy != 0 && policy != 1)) return IVM_EINVAL;
+  if (n > kLongMaxDigits || batch > (size_t)0x7fffffff) return IVM_EUNSUPPORTED;
+  if (c->sticky) return c->sticky;
+  if (cudaSetDevice(c->device) != cudaSuccess) return cuda_fail(c);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t al = 256;
+  auto up = [&](size_t x) { return (x + al - 1) / al * al; };
+  // scratch: cert | idx0 | idx1 | count | a', b' [batch][n] | prod' [batch][2n] | long-multiplication sums
+  const size_t o_i0 = up(batch), o_i1 = o_i0 + up(4 * batch), o_cnt = o_i1 + up(4 * batch);
+  const size_t o_a = o_cnt + al, o_b = o_a + up(batch * n), o_p = o_b + up(batch * n), o_l = o_p + up(2 * n * batch);
+  int r = ensure_lscratch(c, o_l + long_chunk(n, batch) * (2 * n - 1) * 8);
+  if (r) return r;
+  char *L = (char *)c->lscratch;
+  uint8_t *cert = (uint8_t *)L, *ga = (uint8_t *)(L + o_a), *gb = (uint8_t *)(L + o_b), *gp = (uint8_t *)(L + o_p);
+  int *idx0 = (int *)(L + o_i0), *idx1 = (int *)(L + o_i1), *cnt = (int *)(L + o_cnt);
+  int launches = 0, count = (int)batch, h = 0;
+  const int *map = nullptr;  // compact index -> pair (null: identity)
+  const bool f32 = policy == 0 && n <= 32;
+  // policy 1: below m = 1024 the exact long multiplication outruns the interval
+  // FFT on B200 (tools/long_vs_fft.py), so those sizes go to it directly
+  const bool fft = n <= ivm_max_digits(IVM_F64) && !(policy == 1 && ivm_fft_length(n) < 1024);
+  if (fft) {
+    // tier 1: fp32 (n <= 32) or fp64 interval FFT on the whole batch
+    r = ivm_multiply_batched(c, a, b, n, batch, prod, cert, f32 ? IVM_F32 : IVM_F64, stream);
+    if (r) return r;
+    launches += c->last_launches;
+    if (cudaMemsetAsync(cnt, 0, 4, s) != cudaSuccess) return cuda_fail(c);
+    if (ivm::esc_mark(cert, nullptr, count, f32 ? 1 : 2, method, idx0, cnt, s) != 0) return cuda_fail(c);
+    launches++;
+    if (cudaMemcpyAsync(&h, cnt, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess)
+      return cuda_fail(c);
+    count = h;
+    map = idx0;
+    if (f32 && count > 0) {  // tier 2: fp64 for the pairs fp32 did not certify
+      if (ivm::esc_gather(a, n, idx0, count, ga, s) || ivm::esc_gather(b, n, idx0, count, gb, s))
+        return cuda_fail(c);
+      r = ivm_multiply_batched(c, ga, gb, n, (size_t)count, gp, cert, IVM_F64, stream);
+      if (r) return r;
+      launches += 2 + c->last_launches;
+      if (ivm::esc_scatter(gp, 2 * n, idx0, cert, count, prod, s) != 0) return cuda_fail(c);
+      if (cudaMemsetAsync(cnt, 0, 4, s) != cudaSuccess) return cuda_fail(c);
+      if (ivm::esc_mark(cert, idx0, count, 2, method, idx1, cnt, s) != 0) return cuda_fail(c);
+      launches += 2;
+      if (cudaMemcpyAsync(&h, cnt, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+          cudaStreamSynchronize(s) != cudaSuccess)
+        return cuda_fail(c);
+      count = h;
+      map = idx1;
+    }
+  }
+  if (count > 0) {  // tier 3: exact long multiplication
+    const uint8_t *la = a, *lb = b;
+    uint8_t *lp = prod;
+    if (map) {
+      if (ivm::esc_gather(a, n, map, count, ga, s) || ivm::esc_gather(b, n, map, count, gb, s))
+        return cuda_fail(c);
+      launches += 2;
+      la = ga, lb = gb, lp = gp;
+    }
+    r = long_run(c, la, lb, n, (size_t)count, lp, s, o_l, &launches);
+    if (r) return r;
+    if (map) {
+      if (ivm::esc_scatter(gp, 2 * n, map, nullptr, count, prod, s) != 0) return cuda_fail(c);
+      launches++;
+    }
+    if (method) {
+      if (ivm::esc_set_method(map, count, 3, method, s) != 0) return cuda_fail(c);
+      launches++;
+    }
+  }
   c->last_launches = launches;
   if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_fail(c);
   return IVM_OK;

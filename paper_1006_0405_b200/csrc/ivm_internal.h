@@ -78,4 +78,14 @@ int v5_info(int prec, int m, LaunchInfo *li);
 int v5_launch(int prec, int m, const KParams &kp, const Group5Args &ga, int groups, cudaStream_t s);
 int v3g_launch(int prec, int m, const KParams &kp, const GroupArgs &ga, int grid, cudaStream_t s);
 
+// exact long multiplication and the precision escalation helpers
+int long_launch(const uint8_t *a, const uint8_t *b, int n, int batch, long long *coef, uint8_t *prod,
+                cudaStream_t s);
+int esc_mark(const uint8_t *cert, const int *map, int count, int tier, uint8_t *method, int *idx, int *nidx,
+             cudaStream_t s);
+int esc_set_method(const int *map, int count, int tier, uint8_t *method, cudaStream_t s);
+int esc_gather(const uint8_t *src, size_t len, const int *idx, int count, uint8_t *dst, cudaStream_t s);
+int esc_scatter(const uint8_t *src, size_t len, const int *idx, const uint8_t *ok, int count, uint8_t *dst,
+                cudaStream_t s);
+
 }  // namespace ivm
