@@ -79,18 +79,21 @@ static __device__ __forceinline__ CarryStep carry_step(const Src &src, int nc, i
   return s;
 }
 
-// Carry over the words [kb, ke) of one CTA.  Phase 1 (carry_seg_scan): every
-// warp scans its sub-segment with carry-in 0; returns the CTA's generate (carry
-// out with carry-in 0) and all-propagate bits.  Phase 2 (carry_seg_emit): given
-// the CTA's carry-in, writes the digits of the words.  Every thread of the block
-// calls both (blockDim.x a multiple of 32, <= 1024); CarrySeg lives in shared memory.
+// Carry over the words [kb, ke) by a team of nw warps (warps w0 .. w0+nw-1 of
+// the block; by default the whole block).  Phase 1 (carry_seg_scan): every
+// warp scans its sub-segment with carry-in 0; returns the team's generate
+// (carry out with carry-in 0) and all-propagate bits.  Phase 2 (carry_seg_emit):
+// given the team's carry-in, writes the digits of the words.  Every thread of
+// the block calls both (all teams at once: they contain a __syncthreads);
+// CarrySeg lives in shared memory.
 struct CarrySeg {
   unsigned wg[32], wp[32];
 };
 template <typename Src>
 static __device__ __forceinline__ void carry_seg_scan(const Src &src, int nc, int kb, int ke, CarrySeg &cs,
-                                                      unsigned &gen, unsigned &allp) {
-  const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+                                                      unsigned &gen, unsigned &allp, int w0 = 0, int nw = 0) {
+  const unsigned lane = threadIdx.x & 31;
+  const unsigned nwarps = nw ? (unsigned)nw : blockDim.x >> 5, warp = (threadIdx.x >> 5) - (unsigned)w0;
   const int J = (ke - kb + 32 * (int)nwarps - 1) / (32 * (int)nwarps);
   const int k0 = kb + (int)warp * 32 * J;
   unsigned hp, ep;
@@ -116,14 +119,14 @@ static __device__ __forceinline__ void carry_seg_scan(const Src &src, int nc, in
     ep = s.ov_top;
   }
   if (lane == 0) {
-    cs.wg[warp] = c;
-    cs.wp[warp] = ap ? 1u : 0u;
+    cs.wg[w0 + warp] = c;
+    cs.wp[w0 + warp] = ap ? 1u : 0u;
   }
   __syncthreads();
   unsigned G2 = 0, P2 = 0;
   for (unsigned w = 0; w < nwarps; w++) {
-    G2 |= (cs.wg[w] != 0u ? 1u : 0u) << w;
-    P2 |= (cs.wp[w] != 0u ? 1u : 0u) << w;
+    G2 |= (cs.wg[w0 + w] != 0u ? 1u : 0u) << w;
+    P2 |= (cs.wp[w0 + w] != 0u ? 1u : 0u) << w;
   }
   const unsigned long long S = (unsigned long long)(G2 | P2) + G2;
   gen = (unsigned)(S >> nwarps) & 1u;
@@ -132,14 +135,16 @@ static __device__ __forceinline__ void carry_seg_scan(const Src &src, int nc, in
 
 template <typename Src>
 static __device__ __forceinline__ void carry_seg_emit(const Src &src, int nc, int nout, int kb, int ke,
-                                                      const CarrySeg &cs, unsigned cin, uint8_t *__restrict__ out) {
-  const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+                                                      const CarrySeg &cs, unsigned cin, uint8_t *__restrict__ out,
+                                                      int w0 = 0, int nw = 0) {
+  const unsigned lane = threadIdx.x & 31;
+  const unsigned nwarps = nw ? (unsigned)nw : blockDim.x >> 5, warp = (threadIdx.x >> 5) - (unsigned)w0;
   const int J = (ke - kb + 32 * (int)nwarps - 1) / (32 * (int)nwarps);
   const int k0 = kb + (int)warp * 32 * J;
   unsigned G2 = 0, P2 = 0;
   for (unsigned w = 0; w < nwarps; w++) {
-    G2 |= (cs.wg[w] != 0u ? 1u : 0u) << w;
-    P2 |= (cs.wp[w] != 0u ? 1u : 0u) << w;
+    G2 |= (cs.wg[w0 + w] != 0u ? 1u : 0u) << w;
+    P2 |= (cs.wp[w0 + w] != 0u ? 1u : 0u) << w;
   }
   const unsigned long long S0 = (unsigned long long)(G2 | P2) + G2 + cin;
   unsigned c = (unsigned)((S0 ^ P2) >> warp) & 1u;  // carry into this warp's sub-segment

@@ -204,7 +204,8 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Cert3 cs;
   __shared__ CarrySeg seg;
-  __shared__ unsigned s_link[2];
+  __shared__ unsigned s_chunk[2 * (1 << (M - 13))][2];  // this CTA's chunks: generate, all-propagate
+  __shared__ unsigned s_cin[4];                         // carry into each of the 2C^2 chunks
   __shared__ __align__(8) unsigned long long tbar, dbar;
   Buf<T> st{reinterpret_cast<V *>(smem), reinterpret_cast<V *>(smem) + GL::CAP};
   int32_t *coefL = reinterpret_cast<int32_t *>(smem);  // [2][C][B], aliases the state
@@ -375,33 +376,57 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
       const unsigned long long rp = dsm_ld_u64(dsm_map(&cs.maxrad, (unsigned)p));
       rad = rp > rad ? rp : rad;
     }
-    const int words = (nout + 3) / 4, wc = (words + C - 1) / C;
-    const int kb = min((int)crank * wc, words), ke = min(kb + wc, words);
+    // carry: coefficient chunk ch (B coefficients, B/4 words) lives in CTA ch mod C
+    // at local chunk ch / C, so each CTA carries its own 2C chunks, one team of
+    // 8/C warps per chunk; only the chunks' (generate, all-propagate) bits and
+    // two boundary words per chunk cross the cluster
+    constexpr int NCH = 2 * C, TWP = 16 / NCH, WB = B / 4, NCHT = 2 * C * C;
+    const int lc = (int)(threadIdx.x >> 5) / TWP, w0 = lc * TWP, ch = lc * C + (int)crank;
+    const int tt = (int)threadIdx.x - 32 * w0;  // thread index within the team
+    const int words = (nout + 3) / 4;
+    const int kb = min(ch * WB, words), ke = min(kb + WB, words);
     uint8_t *out = kp.prod + (size_t)pair * nout;
     const CoefCluster<M> src{(unsigned)__cvta_generic_to_shared(coefL)};
     unsigned gen = 0u, allp = 1u;
-    if (ok) carry_seg_scan(src, nc, kb, ke, seg, gen, allp);
-    if (threadIdx.x == 0) {
-      s_link[0] = gen;
-      s_link[1] = allp;
+    if (ok) carry_seg_scan(src, nc, kb, ke, seg, gen, allp, w0, TWP);
+    if (tt == 0) {
+      s_chunk[lc][0] = gen;
+      s_chunk[lc][1] = allp;
     }
-    cluster_sync();  // (4) per-CTA generate / all-propagate published
+    cluster_sync();  // (4) every chunk's generate / all-propagate published
     if (ok) {
-      unsigned Gc = 0u, Pc = 0u;
+      if (threadIdx.x < 32) {  // carries into all chunks: the ballot adder over 2C^2 bits
+        unsigned G[4], P[4];
 #pragma unroll
-      for (int p = 0; p < C; p++) {
-        Gc |= (dsm_ld_i32(dsm_map(&s_link[0], (unsigned)p)) != 0 ? 1u : 0u) << p;
-        Pc |= (dsm_ld_i32(dsm_map(&s_link[1], (unsigned)p)) != 0 ? 1u : 0u) << p;
+        for (int w = 0; w < 4; w++) {
+          const int q = 32 * w + (int)threadIdx.x;
+          bool g = false, pq = true;
+          if (q < NCHT) {
+            g = dsm_ld_i32(dsm_map(&s_chunk[q / C][0], (unsigned)(q % C))) != 0;
+            pq = dsm_ld_i32(dsm_map(&s_chunk[q / C][1], (unsigned)(q % C))) != 0;
+          }
+          G[w] = __ballot_sync(0xffffffffu, g);
+          P[w] = __ballot_sync(0xffffffffu, pq);
+        }
+        if (threadIdx.x == 0) {
+          unsigned long long cy = 0ull;
+#pragma unroll
+          for (int w = 0; w < 4; w++) {
+            const unsigned long long S = (unsigned long long)(G[w] | P[w]) + G[w] + cy;
+            s_cin[w] = (unsigned)S ^ P[w];
+            cy = S >> 32;
+          }
+        }
       }
-      const unsigned cin = ((((Gc | Pc) + Gc) ^ Pc) >> crank) & 1u;
-      carry_seg_emit(src, nc, nout, kb, ke, seg, cin, out);
+      __syncthreads();
+      const unsigned cin = (s_cin[ch >> 5] >> (ch & 31)) & 1u;
+      carry_seg_emit(src, nc, nout, kb, ke, seg, cin, out, w0, TWP);
     } else {
-      for (int i = 4 * kb + (int)threadIdx.x; i < min(4 * ke, nout); i += blockDim.x) out[i] = 0;
+      for (int i = 4 * kb + tt; i < min(4 * ke, nout); i += 32 * TWP) out[i] = 0;
     }
     if (kp.coeffs) {
       int64_t *co = kp.coeffs + (size_t)pair * nc;
-      for (int i = 4 * kb + (int)threadIdx.x; i < min(4 * ke, nc); i += blockDim.x)
-        co[i] = ok ? (int64_t)src.one(i) : 0;
+      for (int i = 4 * kb + tt; i < min(4 * ke, nc); i += 32 * TWP) co[i] = ok ? (int64_t)src.one(i) : 0;
     }
     if (crank == 0 && threadIdx.x == 0) {
       kp.cert[pair] = ok ? 1 : 0;
