@@ -90,6 +90,12 @@ __device__ __forceinline__ unsigned cluster_rank() {
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// split barrier: arrive (no memory ordering: the remote reads it guards have
+// been consumed) now, wait later
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 __device__ __forceinline__ unsigned dsm_map(const void *p, unsigned cta) {
   const unsigned a = (unsigned)__cvta_generic_to_shared(p);
   unsigned r;
@@ -155,7 +161,7 @@ template <int M> struct CoefCluster {
 // 4096 columns; x >= 0 is a point, so [x th.lo, x th.hi] needs no sign cases
 template <typename T, int M>
 __device__ __forceinline__ void cross_fwd(const uint8_t *__restrict__ dig, int n, Buf<T> st, const CI<T> *theta,
-                                          unsigned crank) {
+                                          unsigned crank, bool wait_cluster = false) {
   constexpr int C = G4<M>::C;
   const int t = threadIdx.x;
   CI<T> acc[8];
@@ -175,6 +181,7 @@ __device__ __forceinline__ void cross_fwd(const uint8_t *__restrict__ dig, int n
     }
   }
   const bool odd = (crank & 1u) != 0u;
+  if (wait_cluster) cluster_wait();  // the previous pair's remote reads of this state are done
 #pragma unroll
   for (int j = 0; j < 8; j++) st.st(t + 512 * j, odd ? cconj(acc[j]) : acc[j]);
 }
@@ -257,7 +264,8 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
 #pragma unroll 1
     for (int op = 0; op < 2; op++) {
       if (staged) mbar_wait(&dbar, (unsigned)op);
-      cross_fwd<T, M>(staged ? sdig : (op == 0 ? kp.a : kp.b) + (size_t)pair * n, n, st, theta, crank);
+      cross_fwd<T, M>(staged ? sdig : (op == 0 ? kp.a : kp.b) + (size_t)pair * n, n, st, theta, crank,
+                      op == 0 && it > 0);
       if (op == 1 && threadIdx.x == 0) {
         cs.ok = 1;
         cs.first_bad = 0x7fffffff;
@@ -433,8 +441,11 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
       if (kp.max_radius) kp.max_radius[pair] = __longlong_as_double((long long)rad);
       if (kp.first_bad) kp.first_bad[pair] = ok ? -1 : bad;
     }
-    cluster_sync();  // (5) remote coefficient reads done before the next pair overwrites them
+    // (5) remote coefficient / chunk-bit reads done before the next pair
+    // overwrites them: arrive now, wait just before the next state write
+    cluster_arrive_relaxed();
   }
+  if (it > 0) cluster_wait();  // no CTA leaves while its shared memory may still be read
 }
 
 }  // namespace v4
