@@ -140,8 +140,8 @@ int ivm_long_multiply_batched(ivm_ctx_t ctx, const uint8_t *a, const uint8_t *b,
  * n <= 32, else the fp64 one; the fp64 interval FFT for the pairs fp32 did not
  * certify; exact long multiplication for the pairs fp64 did not certify (and
  * for n > ivm_max_digits(IVM_F64)).  policy 1 (fastest exact): long
- * multiplication when the FFT length is below 1024 (where it is faster on
- * B200), else fp64 then long multiplication.
+ * multiplication when the FFT length is below 64 (n <= 16, where it is faster
+ * on B200), else fp64 then long multiplication.
  * prod: device [batch][2n], always the exact product.  method: device
  * [batch] or NULL; receives 1 (fp32 interval), 2 (fp64 interval) or 3 (long
  * multiplication) per pair.  Synchronises `cuda_stream` (the uncertified

@@ -184,7 +184,7 @@ class Context:
     def multiply_exact(self, a, b, out=None, method=None, policy: int = 0, stream=None):
         """Exact products with the fp32 -> fp64 -> long-multiplication
         escalation (policy 1: long multiplication directly below
-        m = 1024); returns (products [B][2n] u8, method [B] u8:
+        m = 64); returns (products [B][2n] u8, method [B] u8:
         1 fp32 interval, 2 fp64 interval, 3 long multiplication)."""
         import torch
         B, n = a.shape

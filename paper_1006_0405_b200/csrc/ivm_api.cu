@@ -169,6 +169,9 @@ static int get_table(ivm_ctx_t c, int m, int prec, const void **out) {
 }
 
 static bool use_v3(ivm_ctx_t c, int m) { return !c->force_v1 && m >= 10 && m <= 13; }
+// fp64 only: at fp32 (C4, the precision-limit sweep) the v1 kernel's full-interval
+// twiddles give ~2x tighter enclosures (93 % vs 0 % of 32-digit uniform pairs certified)
+static bool use_v6(ivm_ctx_t c, int m, int prec) { return !c->force_v1 && prec == IVM_F64 && m >= 6 && m <= 9; }
 static bool use_v4(ivm_ctx_t c, int m) { return !c->force_v3g && m >= 14 && m <= 16; }
 static bool use_v5(ivm_ctx_t c, int m) { return !c->force_v3g && (m == 17 || m == 18); }
 static bool use_v3g(ivm_ctx_t c, int m) { return m >= 14 && m <= 18 && !use_v4(c, m) && !use_v5(c, m); }
@@ -227,7 +230,7 @@ static int get_info4(ivm_ctx_t c, int m, int prec, ivm::LaunchInfo *li) {
 }
 
 static int get_table3(ivm_ctx_t c, int m, int prec, const void **out) {
-  const int radix = (m >= 10 && m <= 13) ? c->radix : 16;
+  const int radix = (m >= 6 && m <= 13) ? 8 : 16;  // v6 / v3 radix-8 plans; v3g radix 16
   auto key = std::make_pair(m * 100 + radix, prec);
   auto it = c->tw3.find(key);
   if (it != c->tw3.end()) {
@@ -263,6 +266,20 @@ static int get_info3(ivm_ctx_t c, int m, int prec, ivm::LaunchInfo *li) {
   if (r == -4) return IVM_EUNSUPPORTED;
   if (r != 0 || li->blocks_per_sm < 1) return cuda_fail(c);
   c->info3[key] = *li;
+  return IVM_OK;
+}
+
+static int get_info6(ivm_ctx_t c, int m, int prec, ivm::LaunchInfo *li) {
+  auto key = std::make_pair(m + 200, prec);
+  auto it = c->info4.find(key);
+  if (it != c->info4.end()) {
+    *li = it->second;
+    return IVM_OK;
+  }
+  int r = ivm::v6_info(prec, m, li);
+  if (r == -4) return IVM_EUNSUPPORTED;
+  if (r != 0 || li->blocks_per_sm < 1) return cuda_fail(c);
+  c->info4[key] = *li;
   return IVM_OK;
 }
 
@@ -320,6 +337,16 @@ int ivm_reserve(ivm_ctx_t c, size_t n, size_t batch, int prec) {
     if (r) return r;
     size_t cl = (size_t)li.max_clusters < batch ? (size_t)li.max_clusters : batch;
     return ensure_scratch(c, cl * li.cluster * li.a_bytes_per_cta);
+  }
+  if (use_v6(c, m, prec)) {
+    const void *t3;
+    ivm::LaunchInfo li;
+    int r = get_table3(c, m, prec, &t3);
+    if (!r) r = get_info6(c, m, prec, &li);
+    if (r) return r;
+    size_t grid = (batch + li.cluster - 1) / li.cluster, cap = (size_t)c->sms * li.blocks_per_sm;
+    if (grid > cap) grid = cap;
+    return ensure_scratch(c, grid * li.a_bytes_per_cta);
   }
   if (use_v5(c, m)) {
     const void *t4;
@@ -394,6 +421,22 @@ int ivm_multiply_batched_diag(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, s
     kp.ascratch = c->ascratch;
     kp.tw = tw;
     if (ivm::v4_launch(prec, m, kp, (int)cl, s) != 0) return cuda_fail(c);
+    c->last_launches = launches + 1;
+    return IVM_OK;
+  }
+  if (use_v6(c, m, prec)) {
+    const void *tw;
+    ivm::LaunchInfo li;
+    r = get_table3(c, m, prec, &tw);
+    if (!r) r = get_info6(c, m, prec, &li);
+    if (r) return r;
+    size_t grid = (batch + li.cluster - 1) / li.cluster, cap = (size_t)c->sms * li.blocks_per_sm;
+    if (grid > cap) grid = cap;
+    r = ensure_scratch(c, grid * li.a_bytes_per_cta);
+    if (r) return r;
+    kp.ascratch = c->ascratch;
+    kp.tw = tw;
+    if (ivm::v6_launch(prec, m, kp, (int)grid, s) != 0) return cuda_fail(c);
     c->last_launches = launches + 1;
     return IVM_OK;
   }
@@ -639,9 +682,9 @@ int ivm_multiply_exact(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, size_t n
   int launches = 0, count = (int)batch, h = 0;
   const int *map = nullptr;  // compact index -> pair (null: identity)
   const bool f32 = policy == 0 && n <= 32;
-  // policy 1: below m = 1024 the exact long multiplication outruns the interval
-  // FFT on B200 (tools/long_vs_fft.py), so those sizes go to it directly
-  const bool fft = n <= ivm_max_digits(IVM_F64) && !(policy == 1 && ivm_fft_length(n) < 1024);
+  // policy 1: below m = 64 (n <= 16) the exact long multiplication outruns the
+  // interval FFT on B200 (tools/long_vs_fft.py), so those sizes go to it directly
+  const bool fft = n <= ivm_max_digits(IVM_F64) && !(policy == 1 && ivm_fft_length(n) < 64);
   if (fft) {
     // tier 1: fp32 (n <= 32) or fp64 interval FFT on the whole batch
     r = ivm_multiply_batched(c, a, b, n, batch, prod, cert, f32 ? IVM_F32 : IVM_F64, stream);

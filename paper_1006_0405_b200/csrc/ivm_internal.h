@@ -44,6 +44,9 @@ int v3_table_entries(int m, int radix);
 int v3_tables(int m, int prec, int radix, const void *w2N, void *out);
 int v3_info(int prec, int m, int radix, LaunchInfo *li);
 int v3_launch(int prec, int m, int radix, const KParams &kp, int grid, cudaStream_t s);
+// small m (2^6 .. 2^9): 8192/m multiplications per 512-thread CTA
+int v6_info(int prec, int m, LaunchInfo *li);
+int v6_launch(int prec, int m, const KParams &kp, int grid, cudaStream_t s);
 // large m (2^14 .. 2^18): one group of C co-resident CTAs per multiplication
 struct GroupInfo {
   int blocks_per_sm;

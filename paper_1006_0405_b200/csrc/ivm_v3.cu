@@ -9,6 +9,7 @@
 #include "ivm_carry.cuh"
 #include "ivm_v3.cuh"
 #include "ivm_v3g.cuh"
+#include "ivm_v6.cuh"
 #include "ivm_twc_host.h"
 
 namespace ivm {
@@ -180,6 +181,46 @@ template <int M> static int v3g_launch_m(int prec, const KParams &kp, const Grou
 }
 int v3g_launch(int prec, int m, const KParams &kp, const GroupArgs &ga, int grid, cudaStream_t s) {
   IVM_V3_DISPATCH(v3g_launch_m, prec, kp, ga, grid, s)
+}
+
+// ---- small m (2^6 .. 2^9): one multiplication per m/16 lanes ----
+template <typename T, int M> static int v6_info_impl(LaunchInfo *li) {
+  using C = v6::Cfg6<T, M>;
+  auto k = v6::ivm_v6_kernel<T, M>;
+  li->threads = C::THREADS;
+  li->smem = C::SMEM;
+  li->a_smem = false;
+  li->a_bytes_per_cta = C::A_BYTES;
+  li->cluster = C::PPC;  // multiplications per CTA
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) != cudaSuccess) return -1;
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, C::THREADS, C::SMEM) != cudaSuccess) return -1;
+  li->blocks_per_sm = nb;
+  return 0;
+}
+template <int M> static int v6_info_m(int prec, LaunchInfo *li) {
+  if constexpr (M < 6 || M > 9) {
+    return -4;
+  } else {
+    return prec == 0 ? v6_info_impl<double, M>(li) : v6_info_impl<float, M>(li);
+  }
+}
+int v6_info(int prec, int m, LaunchInfo *li) { IVM_V3_DISPATCH(v6_info_m, prec, li) }
+
+template <typename T, int M> static void v6_go(const KParams &kp, int grid, cudaStream_t s) {
+  using C = v6::Cfg6<T, M>;
+  v6::ivm_v6_kernel<T, M><<<grid, C::THREADS, C::SMEM, s>>>(kp);
+}
+template <int M> static int v6_launch_m(int prec, const KParams &kp, int grid, cudaStream_t s) {
+  if constexpr (M < 6 || M > 9) {
+    return -4;
+  } else {
+    (prec == 0 ? v6_go<double, M> : v6_go<float, M>)(kp, grid, s);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
+  }
+}
+int v6_launch(int prec, int m, const KParams &kp, int grid, cudaStream_t s) {
+  IVM_V3_DISPATCH(v6_launch_m, prec, kp, grid, s)
 }
 
 }  // namespace ivm

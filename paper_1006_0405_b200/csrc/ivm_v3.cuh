@@ -55,6 +55,12 @@ __host__ __device__ constexpr Plan plan(int m) {
 __host__ __device__ constexpr Plan plan_cta(int m, int R) {
   if (R != 8) return plan(m);
   switch (m) {
+    // warp-per-multiplication kernel (ivm_v6.cuh)
+    case 6: return Plan{3, {2, 4, 8, 0, 0, 0}, 2, {8, 4, 0, 0, 0, 0}};
+    case 7: return Plan{3, {2, 8, 8, 0, 0, 0}, 2, {8, 8, 0, 0, 0, 0}};
+    case 8: return Plan{4, {2, 2, 8, 8, 0, 0}, 3, {8, 8, 2, 0, 0, 0}};
+    case 9: return Plan{4, {2, 4, 8, 8, 0, 0}, 3, {8, 8, 4, 0, 0, 0}};
+    // one-CTA kernel
     case 10: return Plan{4, {2, 8, 8, 8, 0, 0}, 3, {8, 8, 8, 0, 0, 0}};
     case 11: return Plan{5, {2, 2, 8, 8, 8, 0}, 4, {8, 8, 8, 2, 0, 0}};
     case 12: return Plan{5, {2, 4, 8, 8, 8, 0}, 4, {8, 8, 8, 4, 0, 0}};
@@ -315,15 +321,15 @@ template <typename T> struct Buf {
 // G_2[2r][v] = sum_q w_R^{qr} (w_{4R}^q x[v + S'q]), stored with the mirror.
 template <typename T, int M, int RK>
 __device__ __forceinline__ void fwd_first(const uint8_t *__restrict__ dig, int n, Buf<T> st,
-                                          const TwC<T> *__restrict__ tw) {
+                                          const TwC<T> *__restrict__ tw, int tid = threadIdx.x) {
   using Gm = G3<M, RK>;
   constexpr int N = Gm::N, R = Gm::P.f[1], L = 2, S = N / 2, Sp = S / R, G = RK / R;
   constexpr int RSo = Gm::fRS(2), SWo = Gm::fSW(2);
   CI<T> v[G][R];
 #pragma unroll
   for (int g = 0; g < G; g++) {
-    const int nu = threadIdx.x + g * Gm::THREADS;
-    if (Gm::THREADS * G == Sp || nu < Sp) {
+    const int nu = tid + g * Gm::TASKS;  // TASKS threads per multiplication
+    if (Gm::TASKS * G == Sp || nu < Sp) {
 #pragma unroll
       for (int q = 0; q < R; q++) {
         const int idx = nu + Sp * q;
@@ -352,7 +358,7 @@ template <typename T, int M, int RK, int p>
 __device__ __forceinline__ void inv_load_compute(Buf<T> st, const TwC<T> *__restrict__ tw,
                                                  CI<T> (&v)[RK / G3<M, RK>::P.q[p]][G3<M, RK>::P.q[p]],
                                                  int (&k0s)[RK / G3<M, RK>::P.q[p]],
-                                                 int (&nus)[RK / G3<M, RK>::P.q[p]]) {
+                                                 int (&nus)[RK / G3<M, RK>::P.q[p]], int tid = threadIdx.x) {
   using Gm = G3<M, RK>;
   constexpr int N = Gm::N, Q = Gm::P.q[p], L = iL(Gm::P, p), S = N / L, Sp = S / Q, G = RK / Q;
   constexpr int H = Sp / 2, RSi = Gm::iRS(p), SWi = Gm::iSW(p);
@@ -360,11 +366,11 @@ __device__ __forceinline__ void inv_load_compute(Buf<T> st, const TwC<T> *__rest
   constexpr int COUNT = L * H;
 #pragma unroll
   for (int g = 0; g < G; g++) {
-    const int t = threadIdx.x + g * Gm::THREADS;
+    const int t = tid + g * Gm::TASKS;
     const int k0 = t / H, nu = t % H;
-    k0s[g] = (Gm::THREADS * G == COUNT || t < COUNT) ? k0 : -1;
+    k0s[g] = (Gm::TASKS * G == COUNT || t < COUNT) ? k0 : -1;
     nus[g] = nu;
-    if (!(Gm::THREADS * G == COUNT || t < COUNT)) continue;
+    if (!(Gm::TASKS * G == COUNT || t < COUNT)) continue;
 #pragma unroll
     for (int q = 0; q < Q; q++) {
       CI<T> z;
@@ -458,16 +464,18 @@ __device__ __forceinline__ void emit_fold(const CI<T> &o, int r, int k, int n, i
   certify_real(DR<T>::mul_rd(v.il, s), DR<T>::mul_ru(v.ih, s), k + N / 2, n, d1, acc, dump);
 }
 
-template <typename T, int M, int RK>
+template <typename T, int M, int RK, bool WARP = false>
 __device__ __forceinline__ void inv_last(Buf<T> st, const TwC<T> *__restrict__ tw, int n, int32_t *coef,
-                                         CertAcc &acc, double *dump) {
+                                         CertAcc &acc, double *dump, int tid = threadIdx.x) {
   using Gm = G3<M, RK>;
   constexpr int p = Gm::P.ni - 1, Q = Gm::P.q[p], L = iL(Gm::P, p), G = RK / Q;
   constexpr int TWF = Gm::tw_fin();
   CI<T> v[G][Q];
   int k0s[G], nus[G];
-  inv_load_compute<T, M, RK, p>(st, tw, v, k0s, nus);
-  __syncthreads();  // every input loaded: the coefficients may overwrite the state
+  inv_load_compute<T, M, RK, p>(st, tw, v, k0s, nus, tid);
+  // every input loaded: the coefficients may overwrite the state
+  if constexpr (WARP) __syncwarp();
+  else __syncthreads();
 #pragma unroll
   for (int g = 0; g < G; g++) {
     if (k0s[g] < 0) continue;
@@ -538,8 +546,8 @@ __device__ __forceinline__ PassRT pick_inv(int i) {
 // forward: F_p[k0][nu + Sp q] * w_{2LR}^{q(2k0+1)} -> R-point DFT
 template <typename T, int R>
 __device__ __forceinline__ void fwdR(Buf<T> st, const TwC<T> *twb, const PassRT &pp, CI<T> (&v)[R], int &k0,
-                                     int &nu) {
-  const int t = threadIdx.x, Sp = 1 << pp.lgSp;
+                                     int &nu, int t = threadIdx.x) {
+  const int Sp = 1 << pp.lgSp;
   k0 = t >> pp.lgSp;
   nu = t & (Sp - 1);
   const int base = k0 * pp.RSi, sw = k0 & pp.SWi, tstride = pp.L >> 1;
@@ -560,8 +568,8 @@ __device__ __forceinline__ void fwdR(Buf<T> st, const TwC<T> *twb, const PassRT 
 // inverse: E_p[k0][mu] (mirror for q >= R/2) * twiddle -> R-point inverse DFT
 template <typename T, int R, bool FOLD>
 __device__ __forceinline__ void invR(Buf<T> st, const TwC<T> *twb, const PassRT &pp, CI<T> (&v)[R], int &k0,
-                                     int &nu) {
-  const int t = threadIdx.x, Sp = 1 << pp.lgSp, lgH = pp.lgSp - 1, S = R * Sp;
+                                     int &nu, int t = threadIdx.x) {
+  const int Sp = 1 << pp.lgSp, lgH = pp.lgSp - 1, S = R * Sp;
   k0 = t >> lgH;
   nu = t & ((Sp >> 1) - 1);
   const int base = k0 * pp.RSi, sw = k0 & pp.SWi;

@@ -87,16 +87,16 @@ def test_multiply_exact_escalation(ctx, n):
     print("n", n, "methods", np.bincount(method, minlength=4)[1:])
 
 
-@pytest.mark.parametrize("n", [8, 100, 300, 600])
+@pytest.mark.parametrize("n", [8, 16, 17, 100, 600])
 def test_multiply_exact_fastest_policy(ctx, n):
-    """policy 1: long multiplication below m = 1024, fp64 first above; exact."""
+    """policy 1: long multiplication below m = 64, fp64 first above; exact."""
     import torch
     import paper_1006_0405_b200 as ivm
     B = 40
     a, b = inputs.pair_digits(0xE5E + n, np.arange(B), n, kinds_mix(B))
     out, method = ctx.multiply_exact(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), policy=1)
     assert np.array_equal(out.cpu().numpy(), oracle.long_multiply(a, b))
-    want = 3 if ivm.fft_length(n) < 1024 else 2
+    want = 3 if ivm.fft_length(n) < 64 else 2
     assert (method.cpu().numpy() == want).all()
 
 
