@@ -15,7 +15,8 @@ __all__ = ["lib", "Context", "IvmError", "F64", "F32", "fft_length", "max_digits
 
 F64, F32 = 0, 1
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libivm.so")
+# IVM_LIB: an alternative build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("IVM_LIB") or os.path.join(_HERE, "libivm.so")
 
 # every symbol include/ivm.h declares
 EXPORTS = ["ivm_version", "ivm_strerror", "ivm_max_digits", "ivm_fft_length", "ivm_create",
