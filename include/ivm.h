@@ -150,6 +150,16 @@ int ivm_long_multiply_batched(ivm_ctx_t ctx, const uint8_t *a, const uint8_t *b,
 int ivm_multiply_exact(ivm_ctx_t ctx, const uint8_t *a, const uint8_t *b, size_t n, size_t batch,
                        uint8_t *prod, uint8_t *method, int policy, void *cuda_stream);
 
+/* The paper's naive fixed-precision SS: the same FFT
+ * multiplication with punctual complex numbers, round-to-nearest arithmetic
+ * and twiddles, coefficients rounded to the nearest integer.  NOT guaranteed
+ * to be correct -- a speed and error-rate comparator for the certified
+ * path.  a, b: device [batch][n]; prod: device [batch][2n].  prec IVM_F64 or
+ * IVM_F32; n <= 4096 (IVM_EUNSUPPORTED otherwise).  Asynchronous on
+ * `cuda_stream`. */
+int ivm_multiply_naive(ivm_ctx_t ctx, const uint8_t *a, const uint8_t *b, size_t n, size_t batch,
+                       uint8_t *prod, int prec, void *cuda_stream);
+
 /* Seeded synthetic digits on the device (the counter-based SplitMix64
  * generator of SURVEY.md §8(d.2); same bits as
  * paper_1006_0405_b200/inputs.py).  kind: 0 uniform, 1 all-255, 2 sparse

@@ -23,7 +23,7 @@ EXPORTS = ["ivm_version", "ivm_strerror", "ivm_max_digits", "ivm_fft_length", "i
            "ivm_destroy", "ivm_reserve", "ivm_multiply", "ivm_multiply_batched",
            "ivm_multiply_batched_diag", "ivm_multiply_batched_host", "ivm_generate_digits",
            "ivm_peak_probe", "ivm_last_launch_count", "ivm_twiddle_table", "ivm_long_multiply_batched",
-           "ivm_multiply_exact"]
+           "ivm_multiply_exact", "ivm_multiply_naive"]
 
 
 class IvmError(RuntimeError):
@@ -65,6 +65,7 @@ def lib():
         L.ivm_twiddle_table.argtypes = [I, I, P]
         L.ivm_long_multiply_batched.argtypes = [P, P, P, S, S, P, P]
         L.ivm_multiply_exact.argtypes = [P, P, P, S, S, P, P, I, P]
+        L.ivm_multiply_naive.argtypes = [P, P, P, S, S, P, I, P]
         _lib = L
     return _lib
 
@@ -171,6 +172,17 @@ class Context:
                "ivm_multiply_batched_diag")
         return {"prod": out, "cert": cert, "max_radius": rad, "first_bad": bad, "coeffs": co,
                 "intervals": iv, "m": m}
+
+    def multiply_naive(self, a, b, prec: int = F64, out=None, stream=None):
+        """The paper's naive (punctual, round-to-nearest) SS: [B][2n] u8,
+        NOT guaranteed correct."""
+        import torch
+        B, n = a.shape
+        if out is None:
+            out = torch.empty((B, 2 * n), dtype=torch.uint8, device=a.device)
+        _check(lib().ivm_multiply_naive(self._h, _ptr(a), _ptr(b), n, B, _ptr(out), prec, _stream(stream)),
+               "ivm_multiply_naive")
+        return out
 
     def long_multiply(self, a, b, out=None, stream=None):
         """Exact long multiplication on the device: [B][2n] u8."""

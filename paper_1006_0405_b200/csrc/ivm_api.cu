@@ -28,6 +28,9 @@ struct ivm_ctx {
   bool force_v3g = false;  // IVM_KERNEL=v3g: the older global-state group kernel for every m >= 2^14
   std::map<std::pair<int, int>, void *> tw4;  // (log2m, prec) -> v4 role tables
   std::map<std::pair<int, int>, ivm::LaunchInfo> info4;
+  std::map<std::pair<int, int>, void *> twn;  // (log2m, prec) -> round-to-nearest twiddles (naive SS)
+  void *nscratch = nullptr;                  // naive SS: per-CTA spectrum of a
+  size_t nscratch_bytes = 0;
   int radix = 8;  // radix of the one-CTA kernel
   void *ascratch = nullptr;
   size_t ascratch_bytes = 0;
@@ -135,6 +138,8 @@ int ivm_destroy(ivm_ctx_t c) {
   for (auto &kv : c->tw) cudaFree(kv.second);
   for (auto &kv : c->tw3) cudaFree(kv.second);
   for (auto &kv : c->tw4) cudaFree(kv.second);
+  for (auto &kv : c->twn) cudaFree(kv.second);
+  cudaFree(c->nscratch);
   cudaFree(c->ascratch);
   cudaFree(c->slot);
   cudaFree(c->stage);
@@ -736,6 +741,43 @@ int ivm_multiply_exact(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, size_t n
   }
   c->last_launches = launches;
   if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_fail(c);
+  return IVM_OK;
+}
+
+int ivm_multiply_naive(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, size_t n, size_t batch, uint8_t *prod,
+                       int prec, void *stream) {
+  if (!c || !a || !b || !prod || n == 0 || batch == 0 || (prec != IVM_F64 && prec != IVM_F32)) return IVM_EINVAL;
+  if (n > 4096 || batch > (size_t)0x7fffffff) return IVM_EUNSUPPORTED;
+  if (c->sticky) return c->sticky;
+  if (cudaSetDevice(c->device) != cudaSuccess) return cuda_fail(c);
+  const int lg = log2m_for(n) < 1 ? 1 : log2m_for(n);
+  auto key = std::make_pair(lg, prec);
+  void *w = nullptr;
+  auto it = c->twn.find(key);
+  if (it != c->twn.end()) {
+    w = it->second;
+  } else {
+    const size_t es = prec == IVM_F64 ? 8 : 4, bytes = ((size_t)2 << lg) * es;
+    std::vector<unsigned char> h(bytes);
+    if (ivm::plan_twiddles_rn(lg, prec, h.data()) != 0) return IVM_EUNSUPPORTED;
+    if (cudaMalloc(&w, bytes) != cudaSuccess) return IVM_ENOMEM;
+    if (cudaMemcpy(w, h.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess) return cuda_fail(c);
+    c->twn[key] = w;
+  }
+  const int smem = ivm::naive_smem(lg, prec);
+  size_t grid = (size_t)c->sms * (smem > 114 * 1024 ? 1 : (smem > 56 * 1024 ? 2 : 4));
+  if (grid > batch) grid = batch;
+  const size_t need = grid * ((size_t)1 << lg) * (prec == IVM_F64 ? 16 : 8);
+  if (c->nscratch_bytes < need) {
+    cudaFree(c->nscratch);
+    c->nscratch = nullptr;
+    c->nscratch_bytes = 0;
+    if (cudaMalloc(&c->nscratch, need) != cudaSuccess) return IVM_ENOMEM;
+    c->nscratch_bytes = need;
+  }
+  if (ivm::naive_launch(prec, a, b, (int)n, (int)batch, lg, w, c->nscratch, prod, (int)grid, (cudaStream_t)stream) != 0)
+    return cuda_fail(c);
+  c->last_launches = 1;
   return IVM_OK;
 }
 

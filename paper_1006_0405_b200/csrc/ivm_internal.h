@@ -38,6 +38,7 @@ int digits_launch(uint8_t *out, int n, long long batch, uint64_t seed, uint64_t 
 int probe_launch(int prec, int iters, void *sink, int sms, cudaStream_t s, uint64_t *count);
 int dump_map_launch(int32_t *slot, int batch, const int32_t *pairs, int n_dump, cudaStream_t s);
 int plan_twiddles(int m, int prec, void *out);
+int plan_twiddles_rn(int m, int prec, void *out);
 // v3 (odd-frequency, balanced) path
 int upload_w64(const double *w64, const float *w32);
 int v3_table_entries(int m, int radix);
@@ -81,6 +82,10 @@ int v5_info(int prec, int m, LaunchInfo *li);
 int v5_launch(int prec, int m, const KParams &kp, const Group5Args &ga, int groups, cudaStream_t s);
 int v3g_launch(int prec, int m, const KParams &kp, const GroupArgs &ga, int grid, cudaStream_t s);
 
+// the naive (punctual, round-to-nearest) SS comparator
+int naive_smem(int lg, int prec);
+int naive_launch(int prec, const uint8_t *a, const uint8_t *b, int n, int batch, int lg, const void *w, void *scratch,
+                 uint8_t *prod, int grid, cudaStream_t s);
 // exact long multiplication and the precision escalation helpers
 int long_launch(const uint8_t *a, const uint8_t *b, int n, int batch, long long *coef, uint8_t *prod,
                 cudaStream_t s);

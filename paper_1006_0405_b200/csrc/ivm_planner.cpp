@@ -105,6 +105,30 @@ template <typename F> int build(int m, F *out /* [N][4] */) {
   return 0;
 }
 
+// nearest-rounded points (cos, sin) of omega_N^j for the naive (punctual) SS
+// comparator: binary128 values rounded to nearest; exact at multiples of pi/2
+template <typename F> int build_rn(int m, F *out /* [N][2] */) {
+  const long N = 1L << m;
+  for (long j = 0; j < N; j++) {
+    F c, s;
+    if (N >= 4 && j % (N / 4) == 0) {
+      const long q = j / (N / 4);
+      c = (q == 0) ? 1 : (q == 2 ? -1 : 0);
+      s = (q == 1) ? 1 : (q == 3 ? -1 : 0);
+    } else if (N < 4) {
+      c = (j == 0) ? 1 : -1;
+      s = 0;
+    } else {
+      const __float128 th = 2 * M_PIq * (__float128)j / (__float128)N;
+      c = (F)cosq(th);
+      s = (F)sinq(th);
+    }
+    out[2 * j] = c;
+    out[2 * j + 1] = s;
+  }
+  return 0;
+}
+
 }  // namespace
 
 namespace ivm {
@@ -112,5 +136,10 @@ namespace ivm {
 int plan_twiddles(int m, int prec, void *out) {
   if (m < 0 || m > 26) return -1;
   return prec == 0 ? build<double>(m, (double *)out) : build<float>(m, (float *)out);
+}
+// prec 0: double[N][2]; prec 1: float[N][2] (round to nearest, no enclosure)
+int plan_twiddles_rn(int m, int prec, void *out) {
+  if (m < 0 || m > 26) return -1;
+  return prec == 0 ? build_rn<double>(m, (double *)out) : build_rn<float>(m, (float *)out);
 }
 }  // namespace ivm
