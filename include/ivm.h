@@ -48,6 +48,7 @@ extern "C" {
 #endif
 
 typedef struct ivm_ctx *ivm_ctx_t;
+typedef struct ivm_multi *ivm_multi_t;  /* G device contexts + NCCL communicators */
 
 enum { IVM_F64 = 0, IVM_F32 = 1 };
 
@@ -57,6 +58,7 @@ enum {
     IVM_ENOMEM = -2,        /* device or host allocation failed */
     IVM_ECUDA = -3,         /* CUDA runtime / launch error (sticky) */
     IVM_EUNSUPPORTED = -4,  /* size / precision not supported by this build */
+    IVM_ENCCL = -5,         /* NCCL missing or failed (multi-GPU API) */
     IVM_ENODEV = -6         /* no CUDA device */
 };
 
@@ -159,6 +161,29 @@ int ivm_multiply_exact(ivm_ctx_t ctx, const uint8_t *a, const uint8_t *b, size_t
  * `cuda_stream`. */
 int ivm_multiply_naive(ivm_ctx_t ctx, const uint8_t *a, const uint8_t *b, size_t n, size_t batch,
                        uint8_t *prod, int prec, void *cuda_stream);
+
+/* Single-process multi-GPU: one context per device plus NCCL
+ * communicators (ncclCommInitAll; NCCL is dlopen'ed, "libnccl.so.2").
+ * devices: [ngpu] CUDA ordinals, devices[0] is the root.  IVM_ENCCL if NCCL
+ * cannot be loaded or initialised.  (One process per GPU under
+ * torch.distributed is the other supported launch model: bench.py.) */
+int ivm_multi_create(ivm_multi_t *m, int ngpu, const int *devices);
+
+/* Independent multiplications sharded by the caller: shard g (device
+ * devices[g]) multiplies a_shards[g], b_shards[g] ([batch_per_gpu][n], device
+ * memory of that GPU) into prod_shards[g] ([batch_per_gpu][2n]) and
+ * cert_shards[g] ([batch_per_gpu]); no data-path collective.  If
+ * gather_to_root, the products and flags are gathered in shard order into
+ * root_prod ([ngpu * batch_per_gpu][2n]) and root_cert ([ngpu *
+ * batch_per_gpu]) on the root device (grouped ncclSend / ncclRecv).  Returns
+ * after every device's work (and the gather) completed. */
+int ivm_multi_multiply(ivm_multi_t m, const uint8_t *const *a_shards, const uint8_t *const *b_shards,
+                       size_t n, size_t batch_per_gpu, uint8_t *const *prod_shards,
+                       uint8_t *const *cert_shards, int prec, int gather_to_root, uint8_t *root_prod,
+                       uint8_t *root_cert);
+
+/* Destroy the communicators and contexts; NULL is a no-op. */
+int ivm_multi_destroy(ivm_multi_t m);
 
 /* Seeded synthetic digits on the device (the counter-based SplitMix64
  * generator of SURVEY.md §8(d.2); same bits as

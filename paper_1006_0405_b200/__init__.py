@@ -23,7 +23,8 @@ EXPORTS = ["ivm_version", "ivm_strerror", "ivm_max_digits", "ivm_fft_length", "i
            "ivm_destroy", "ivm_reserve", "ivm_multiply", "ivm_multiply_batched",
            "ivm_multiply_batched_diag", "ivm_multiply_batched_host", "ivm_generate_digits",
            "ivm_peak_probe", "ivm_last_launch_count", "ivm_twiddle_table", "ivm_long_multiply_batched",
-           "ivm_multiply_exact", "ivm_multiply_naive"]
+           "ivm_multiply_exact", "ivm_multiply_naive", "ivm_multi_create", "ivm_multi_multiply",
+           "ivm_multi_destroy"]
 
 
 class IvmError(RuntimeError):
@@ -66,6 +67,9 @@ def lib():
         L.ivm_long_multiply_batched.argtypes = [P, P, P, S, S, P, P]
         L.ivm_multiply_exact.argtypes = [P, P, P, S, S, P, P, I, P]
         L.ivm_multiply_naive.argtypes = [P, P, P, S, S, P, I, P]
+        L.ivm_multi_create.argtypes = [ctypes.POINTER(P), I, P]
+        L.ivm_multi_multiply.argtypes = [P, P, P, S, S, P, P, I, I, P, P]
+        L.ivm_multi_destroy.argtypes = [P]
         _lib = L
     return _lib
 

@@ -20,10 +20,11 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--ftz=false",
                   "--prec-div=true", "--prec-sqrt=true", "--fmad=true", "-Xptxas", "-v",
                   "-I", os.path.join(ROOT, "include")]
-CXXFLAGS = ["-O2", "-fPIC", "-std=gnu++17", "-fext-numeric-literals", "-I", os.path.join(ROOT, "include")]
+CXXFLAGS = ["-O2", "-fPIC", "-std=gnu++17", "-fext-numeric-literals", "-I", os.path.join(ROOT, "include"),
+            "-I", os.path.join(os.path.dirname(os.path.dirname(NVCC)), "include")]
 
 CU = ["ivm_kernels.cu", "ivm_v3.cu", "ivm_v4.cu", "ivm_v5.cu", "ivm_long.cu", "ivm_naive.cu", "ivm_api.cu"]
-CPP = ["ivm_planner.cpp"]
+CPP = ["ivm_planner.cpp", "ivm_multi.cpp"]
 # every header under csrc/ is a dependency of every translation unit
 HDR = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 
@@ -71,7 +72,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             # fall back to a dynamic libquadmath
-            cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", OUT, *objs, "-lquadmath"]
+            cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", OUT, *objs, "-lquadmath", "-ldl"]
             subprocess.check_call(cmd)
     return OUT
 

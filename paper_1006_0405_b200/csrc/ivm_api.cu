@@ -75,6 +75,7 @@ const char *ivm_strerror(int s) {
     case IVM_ENOMEM: return "out of memory";
     case IVM_ECUDA: return "CUDA error";
     case IVM_EUNSUPPORTED: return "unsupported size or precision";
+    case IVM_ENCCL: return "NCCL unavailable or failed";
     case IVM_ENODEV: return "no CUDA device";
     default: return "unknown status";
   }
