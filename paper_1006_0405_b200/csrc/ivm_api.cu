@@ -458,11 +458,11 @@ int ivm_multiply_batched_diag(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, s
     if (groups < 1) return IVM_EUNSUPPORTED;
     r = ensure_scratch(c, groups * C * li.a_bytes_per_cta);
     if (r) return r;
-    const size_t al = 256, M2 = (size_t)1 << m, es = prec == IVM_F64 ? 8 : 4;
+    const size_t al = 256, es = prec == IVM_F64 ? 8 : 4;
     auto up = [&](size_t x) { return (x + al - 1) / al * al; };
-    const size_t b_x = up(groups * C * 4096 * 4 * es), b_c = up(groups * M2 * 8), b_l = up(groups * C * 32),
-                 b_ctr = up(groups * 4);
-    const size_t need = b_x + b_c + b_l + b_ctr;
+    const size_t b_x = up(groups * C * 4096 * 4 * es), b_l = up(groups * C * 32),
+                 b_b = up(groups * 2 * C * C * 8 * 8), b_bits = up(groups * 2 * C * C), b_ctr = up(groups * 4);
+    const size_t need = b_x + b_l + b_b + b_bits + b_ctr;
     if (c->gscratch_bytes < need) {
       cudaFree(c->gscratch);
       c->gscratch = nullptr;
@@ -473,9 +473,10 @@ int ivm_multiply_batched_diag(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, s
     char *gs = (char *)c->gscratch;
     ivm::Group5Args ga;
     ga.xch = gs;
-    ga.coef = (long long *)(gs + b_x);
-    ga.link = (unsigned *)(gs + b_x + b_c);
-    ga.ctr = (unsigned *)(gs + b_x + b_c + b_l);
+    ga.link = (unsigned *)(gs + b_x);
+    ga.bnd = (long long *)(gs + b_x + b_l);
+    ga.bits = (uint8_t *)(gs + b_x + b_l + b_b);
+    ga.ctr = (unsigned *)(gs + b_x + b_l + b_b + b_bits);
     if (cudaMemsetAsync(ga.ctr, 0, b_ctr, s) != cudaSuccess) return cuda_fail(c);
     kp.ascratch = c->ascratch;
     kp.tw = tw;

@@ -118,6 +118,11 @@ static __device__ __forceinline__ void carry_seg_scan(const Src &src, int nc, in
     hp = s.hi_top;
     ep = s.ov_top;
   }
+  if (nw == 1) {  // a one-warp team: its carry-out is the segment's (no block barrier)
+    gen = c;
+    allp = ap ? 1u : 0u;
+    return;
+  }
   if (lane == 0) {
     cs.wg[w0 + warp] = c;
     cs.wp[w0 + warp] = ap ? 1u : 0u;
@@ -147,7 +152,7 @@ static __device__ __forceinline__ void carry_seg_emit(const Src &src, int nc, in
     P2 |= (cs.wp[w0 + w] != 0u ? 1u : 0u) << w;
   }
   const unsigned long long S0 = (unsigned long long)(G2 | P2) + G2 + cin;
-  unsigned c = (unsigned)((S0 ^ P2) >> warp) & 1u;  // carry into this warp's sub-segment
+  unsigned c = nw == 1 ? cin : (unsigned)((S0 ^ P2) >> warp) & 1u;  // carry into this warp's sub-segment
   unsigned hp, ep;
   {
     unsigned l1, h1, l2, h2;

@@ -74,8 +74,9 @@ int v4_launch(int prec, int m, const KParams &kp, int clusters, cudaStream_t s);
 struct Group5Args {
   unsigned *ctr;   // [groups], zeroed before every launch
   void *xch;       // [groups][C][4096] complex intervals
-  long long *coef;  // [groups][m]
-  unsigned *link;   // [groups][C][8]
+  unsigned *link;  // [groups][C][8]
+  long long *bnd;  // [groups][2 C^2][8]
+  uint8_t *bits;   // [groups][2 C^2]
 };
 int upload_w64_v5(const double *w64, const float *w32);
 int v5_info(int prec, int m, LaunchInfo *li);

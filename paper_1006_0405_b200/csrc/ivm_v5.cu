@@ -59,7 +59,7 @@ int v5_info(int prec, int m, LaunchInfo *li) { IVM_V5_DISPATCH(v5_info_m, prec, 
 template <typename T, int M> static int v5_go(const KParams &kp, const Group5Args &ga, int groups, cudaStream_t s) {
   using CF = v5::Cfg5<T, M>;
   KParams k2 = kp;
-  v5::Group5 g{ga.ctr, ga.xch, ga.coef, ga.link};
+  v5::Group5 g{ga.ctr, ga.xch, ga.link, ga.bnd, ga.bits};
   void *args[] = {(void *)&k2, (void *)&g};
   return cudaLaunchCooperativeKernel((const void *)v5::ivm_v5_kernel<T, M>, dim3(groups * v4::G4<M>::C),
                                      dim3(CF::THREADS), args, CF::SMEM, s) == cudaSuccess

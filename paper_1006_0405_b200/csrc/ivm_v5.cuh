@@ -11,10 +11,13 @@
 //     inverse pass (radix C, untwist folded into the input twiddles) as two
 //     shared-memory stages, C = 8 C2:
 //       out_{r1 + 8 r2} = sum_b w_{C2}^{-b r2} [ w_C^{-b r1} sum_a w_8^{-a r1} y_{C2 a + b} ],
-//     then scales, certifies and snaps c_k, c_{k+m/2} (k = k0 + 4096 r) into a
-//     global int32 coefficient array; barrier;
-//   * carry over contiguous word segments, group-level ballot adder through
-//     global link words; barrier.
+//     then scales, certifies and snaps c_k, c_{k+m/2} (k = k0 + 4096 r) into
+//     its own shared memory (int64: 255^2 n > 2^31 here): chunk ch of B
+//     consecutive coefficients lives in CTA ch mod C; every CTA publishes its
+//     chunks' last 8 coefficients; barrier;
+//   * each CTA carries its own chunks (one warp per chunk) and publishes their
+//     generate / all-propagate bits; barrier; the carries into all 2 C^2 chunks
+//     follow from one ballot adder; digits out.
 #pragma once
 
 namespace ivm {
@@ -26,22 +29,12 @@ using namespace v4;
 struct Group5 {
   unsigned *ctr;   // [groups] barrier counters (zeroed by the host before the launch)
   void *xch;       // [groups][C][4096] CI<T> column exchange
-  long long *coef;  // [groups][m] coefficients (up to 255^2 n > 2^31)
-  unsigned *link;  // [groups][C][8] per-CTA certificate / carry words
+  unsigned *link;  // [groups][C][8] per-CTA certificate words
+  long long *bnd;  // [groups][2 C^2][8] last 8 coefficients of every chunk
+  uint8_t *bits;   // [groups][2 C^2] chunk generate | all-propagate << 1
 };
 
-// coefficients written by other SMs: read through L2 only (no stale L1 lines)
-struct CoefGlobalCG {
-  const long long *c;
-  __device__ __forceinline__ void quad(int k, unsigned long long (&o)[4]) const {
-    const longlong2 a = __ldcg(reinterpret_cast<const longlong2 *>(c) + 2 * k);
-    const longlong2 b = __ldcg(reinterpret_cast<const longlong2 *>(c) + 2 * k + 1);
-    o[0] = (unsigned long long)a.x, o[1] = (unsigned long long)a.y, o[2] = (unsigned long long)b.x,
-    o[3] = (unsigned long long)b.y;
-  }
-  __device__ __forceinline__ unsigned long long one(int i) const { return (unsigned long long)__ldcg(c + i); }
-};
-
+// a complex interval written by another SM: read through L2 only (no stale L1 lines)
 template <typename T> __device__ __forceinline__ CI<T> ldcg_ci(const CI<T> *p) {
   if constexpr (sizeof(T) == 8) {
     const double2 a = __ldcg(reinterpret_cast<const double2 *>(p)), b = __ldcg(reinterpret_cast<const double2 *>(p) + 1);
@@ -51,6 +44,33 @@ template <typename T> __device__ __forceinline__ CI<T> ldcg_ci(const CI<T> *p) {
     return CI<T>{a.x, a.y, a.z, a.w};
   }
 }
+
+template <typename T> __device__ __forceinline__ void st_ci(CI<T> *p, const CI<T> &z) {  // 16-B stores
+  if constexpr (sizeof(T) == 8) {
+    reinterpret_cast<double2 *>(p)[0] = make_double2(z.rl, z.rh);
+    reinterpret_cast<double2 *>(p)[1] = make_double2(z.il, z.ih);
+  } else {
+    *reinterpret_cast<float4 *>(p) = make_float4(z.rl, z.rh, z.il, z.ih);
+  }
+}
+
+// coefficients of one chunk (B consecutive c_i from `first`, shared memory) and
+// the last 8 coefficients of the preceding chunk (global boundary array)
+struct ChunkSrc {
+  const long long *local;
+  const long long *prev8;  // c_{first-8} .. c_{first-1} (shared copy; zeros for the first chunk)
+  int first;
+  __device__ __forceinline__ unsigned long long get(int i) const {
+    // (chunks past the last word prime their empty segment from far below: 0)
+    return i >= first ? (unsigned long long)local[i - first]
+                      : (i >= first - 8 ? (unsigned long long)prev8[i - first + 8] : 0ull);
+  }
+  __device__ __forceinline__ void quad(int k, unsigned long long (&o)[4]) const {
+#pragma unroll
+    for (int e = 0; e < 4; e++) o[e] = get(4 * k + e);
+  }
+  __device__ __forceinline__ unsigned long long one(int i) const { return get(i); }
+};
 
 __device__ __forceinline__ void gsync(unsigned *ctr, unsigned C, unsigned &gen) {
   __syncthreads();
@@ -109,7 +129,6 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
   const int gi = (int)(blockIdx.x / C), ngr = (int)(gridDim.x / C);
   unsigned *ctr = g.ctr + gi;
   CI<T> *xch = reinterpret_cast<CI<T> *>(g.xch) + (size_t)gi * C * 4096;
-  long long *gcoef = g.coef + (size_t)gi * N;
   unsigned *link = g.link + (size_t)gi * C * 8;
   unsigned gen = 0;
   const TwC<T> *tw = reinterpret_cast<const TwC<T> *>(kp.tw);
@@ -202,7 +221,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
         __syncthreads();
       } else {  // last local pass: the column goes to the group's exchange scratch (row k0 + L r)
 #pragma unroll
-        for (int r = 0; r < R; r++) xch[(size_t)crank * 4096 + k0 + pp.L * r] = v[r];
+        for (int r = 0; r < R; r++) st_ci(xch + (size_t)crank * 4096 + k0 + pp.L * r, v[r]);
       }
     }
     __syncthreads();
@@ -237,37 +256,70 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
       __syncthreads();
     }
     CertAcc acc;
-    {  // stage 2: task (r1, kl), DFT_C2 over b, untwist remainder, emit
+    // stage 2: task (r1, kl), DFT_C2 over b, untwist remainder, emit.  The
+    // coefficients go to this CTA's shared memory (int64), chunk ch = (h C + r)
+    // of B consecutive c_i: fp64 into the twiddle swap buffer (free until the
+    // next pair's forward-last table, fetched after the carry), fp32 (whose swap
+    // buffer is too small) into the state once every input is in registers
+    constexpr int TASKS = 8 * B / 512;
+    constexpr bool IN_SWAP = sizeof(TwC<T>) * 4096 >= 8 * 8192;
+    long long *coefL = IN_SWAP ? reinterpret_cast<long long *>(twb + X::S_SWAP) : reinterpret_cast<long long *>(smem);
+    {
       double *dump = diag_dump(kp, pair, N);
-      constexpr int TASKS = 8 * B / 512;
+      if constexpr (IN_SWAP) {
 #pragma unroll
-      for (int g2 = 0; g2 < TASKS; g2++) {
-        const int task = (int)threadIdx.x + 512 * g2, r1 = task / B, kl = task % B;
-        const int k0 = (int)crank * B + kl;
-        CI<T> v[C2];
+        for (int g2 = 0; g2 < TASKS; g2++) {
+          const int task = (int)threadIdx.x + 512 * g2, r1 = task / B, kl = task % B;
+          const int k0 = (int)crank * B + kl;
+          CI<T> v[C2];
 #pragma unroll
-        for (int b = 0; b < C2; b++) v[b] = st.ld((r1 * C2 + b) * B + kl);
-        cdft<T, C2, true>(v);
+          for (int b = 0; b < C2; b++) v[b] = st.ld((r1 * C2 + b) * B + kl);
+          cdft<T, C2, true>(v);
 #pragma unroll
-        for (int r2 = 0; r2 < C2; r2++) {
-          const int r = r1 + 8 * r2, k = k0 + 4096 * r;
-          emit_tab<T, M>(v[r2], fold[r], k, n, gcoef + k, gcoef + k + N / 2, acc, dump);
+          for (int r2 = 0; r2 < C2; r2++) {
+            const int r = r1 + 8 * r2, k = k0 + 4096 * r;
+            emit_tab<T, M>(v[r2], fold[r], k, n, coefL + r * B + kl, coefL + (C + r) * B + kl, acc, dump);
+          }
+        }
+      } else {
+        CI<T> v[TASKS][C2];
+#pragma unroll
+        for (int g2 = 0; g2 < TASKS; g2++) {
+          const int task = (int)threadIdx.x + 512 * g2, r1 = task / B, kl = task % B;
+#pragma unroll
+          for (int b = 0; b < C2; b++) v[g2][b] = st.ld((r1 * C2 + b) * B + kl);
+        }
+        __syncthreads();  // the state is free for the coefficients
+#pragma unroll
+        for (int g2 = 0; g2 < TASKS; g2++) {
+          const int task = (int)threadIdx.x + 512 * g2, r1 = task / B, kl = task % B;
+          const int k0 = (int)crank * B + kl;
+          cdft<T, C2, true>(v[g2]);
+#pragma unroll
+          for (int r2 = 0; r2 < C2; r2++) {
+            const int r = r1 + 8 * r2, k = k0 + 4096 * r;
+            emit_tab<T, M>(v[g2][r2], fold[r], k, n, coefL + r * B + kl, coefL + (C + r) * B + kl, acc, dump);
+          }
         }
       }
     }
     cert_flush(acc, cs);
     __syncthreads();
+    // chunk ch (global, B coefficients from ch B) is local chunk lc = ch / C of CTA ch % C
+    constexpr int NCH = 2 * C, NCHT = 2 * C * C, WB = B / 4, ROUNDS = NCH / 16;
+    long long *bnd = g.bnd + (size_t)gi * NCHT * 8;
+    uint8_t *bits = g.bits + (size_t)gi * NCHT;
+    for (int e = (int)threadIdx.x; e < NCH * 8; e += blockDim.x) {  // boundary words of the own chunks
+      const int lc = e / 8, ch = lc * C + (int)crank;
+      bnd[(size_t)ch * 8 + (e % 8)] = coefL[lc * B + B - 8 + (e % 8)];
+    }
     if (threadIdx.x == 0) {
       link[crank * 8 + 0] = (unsigned)cs.ok;
       link[crank * 8 + 1] = (unsigned)cs.first_bad;
       link[crank * 8 + 2] = (unsigned)(cs.maxrad & 0xffffffffu);
       link[crank * 8 + 3] = (unsigned)(cs.maxrad >> 32);
-      if (pair + ngr < kp.batch) {  // next pair's forward-last table
-        mbar_expect(&tbar, EB * X::FLAST);
-        bulk_copy(twb + X::S_SWAP, tw + X::FWD(crank) + X::FP(4), EB * X::FLAST, &tbar);
-      }
     }
-    gsync(ctr, C, gen);  // (2) coefficients and certificates of every CTA visible
+    gsync(ctr, C, gen);  // (2) certificates and chunk boundaries of every CTA visible
     int ok = 1, bad = 0x7fffffff;
     unsigned long long rad = 0ull;
     for (int p = 0; p < C; p++) {
@@ -277,32 +329,82 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
       const unsigned long long rp = (unsigned long long)lp[2] | ((unsigned long long)lp[3] << 32);
       rad = rp > rad ? rp : rad;
     }
-    const int words = (nout + 3) / 4, wc = (words + C - 1) / C;
-    const int kb = min((int)crank * wc, words), ke = min(kb + wc, words);
+    const int words = (nout + 3) / 4, warp = (int)threadIdx.x >> 5;
     uint8_t *out = kp.prod + (size_t)pair * nout;
-    const CoefGlobalCG src{gcoef};
-    unsigned gn = 0u, ap = 1u;
-    if (ok) carry_seg_scan(src, nc, kb, ke, seg, gn, ap);
-    if (threadIdx.x == 0) {
-      link[crank * 8 + 4] = gn;
-      link[crank * 8 + 5] = ap;
+    __shared__ uint8_t s_cin[64];
+    __shared__ long long s_prev[64][8];  // boundary coefficients before each own chunk
+    for (int e = (int)threadIdx.x; e < NCH * 8; e += blockDim.x) {
+      const int lc = e / 8, ch = lc * C + (int)crank;
+      s_prev[lc][e % 8] = ch > 0 ? __ldcg(bnd + (size_t)(ch - 1) * 8 + e % 8) : 0ll;
     }
-    gsync(ctr, C, gen);  // (3) per-CTA generate / all-propagate visible
+    __syncthreads();
+    // scan: one warp per chunk, ROUNDS chunks per warp
+#pragma unroll 1
+    for (int rd = 0; rd < ROUNDS; rd++) {
+      const int lc = rd * 16 + warp, ch = lc * C + (int)crank;
+      const int kb = min(ch * WB, words), ke = min(kb + WB, words);
+      const ChunkSrc src{coefL + lc * B, s_prev[lc], ch * B};
+      unsigned gn = 0u, ap = 1u;
+      if (ok) carry_seg_scan(src, nc, kb, ke, seg, gn, ap, warp, 1);
+      if ((threadIdx.x & 31) == 0) bits[ch] = (uint8_t)(gn | (ap << 1));
+    }
+    gsync(ctr, C, gen);  // (3) every chunk's generate / all-propagate visible
     if (ok) {
-      // carry into this CTA: scan of (generate, all-propagate) over the CTAs below
-      unsigned cin = 0u;
-      for (unsigned p = 0; p < crank; p++) {
-        const volatile unsigned *lp = link + p * 8;
-        cin = lp[4] | (lp[5] & cin);
+      if (threadIdx.x < 32) {  // carries into all 2C^2 chunks: 64 chunks per lane, then across lanes
+        const int l = (int)threadIdx.x;
+        unsigned long long G = 0ull, P = ~0ull;  // beyond the chunks: propagate
+        if (64 * l < NCHT) {  // NCHT is a multiple of 64: 4 x 16 B per lane
+          P = 0ull;
+          const uint4 *bp = reinterpret_cast<const uint4 *>(bits + 64 * l);
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            const uint4 w = __ldcg(bp + q);
+            const unsigned ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int e = 0; e < 16; e++) {
+              const unsigned bb = (ws[e >> 2] >> (8 * (e & 3))) & 3u;
+              G |= (unsigned long long)(bb & 1u) << (16 * q + e);
+              P |= (unsigned long long)(bb >> 1) << (16 * q + e);
+            }
+          }
+        }
+        const unsigned long long X0 = (G | P) + G;
+        const bool sg = X0 < (G | P), sp = P == ~0ull;  // segment generate / all-propagate
+        const unsigned Gw = __ballot_sync(0xffffffffu, sg), Pw = __ballot_sync(0xffffffffu, sp);
+        const unsigned cinl = ((((Gw | Pw) + Gw) ^ Pw) >> l) & 1u;
+        const unsigned long long cb = ((G | P) + G + cinl) ^ P;  // carry into each chunk of the segment
+        for (int j = 0; j < 64; j++) {
+          const int ch = 64 * l + j;
+          if (ch < NCHT && ch % C == (int)crank) s_cin[ch / C] = (uint8_t)((cb >> j) & 1ull);
+        }
       }
-      carry_seg_emit(src, nc, nout, kb, ke, seg, cin, out);
+      __syncthreads();
+#pragma unroll 1
+      for (int rd = 0; rd < ROUNDS; rd++) {
+        const int lc = rd * 16 + warp, ch = lc * C + (int)crank;
+        const int kb = min(ch * WB, words), ke = min(kb + WB, words);
+        const ChunkSrc src{coefL + lc * B, s_prev[lc], ch * B};
+        // a one-warp team: the carry into the warp is the chunk's carry-in whatever
+        // the (stale) per-warp bits in seg say
+        carry_seg_emit(src, nc, nout, kb, ke, seg, s_cin[lc], out, warp, 1);
+      }
     } else {
-      for (int i = 4 * kb + (int)threadIdx.x; i < min(4 * ke, nout); i += blockDim.x) out[i] = 0;
+      for (int lc = 0; lc < NCH; lc++) {
+        const int ch = lc * C + (int)crank, kb = min(ch * WB, words), ke = min(kb + WB, words);
+        for (int i = 4 * kb + (int)threadIdx.x; i < min(4 * ke, nout); i += blockDim.x) out[i] = 0;
+      }
     }
     if (kp.coeffs) {
       int64_t *co = kp.coeffs + (size_t)pair * nc;
-      for (int i = 4 * kb + (int)threadIdx.x; i < min(4 * ke, nc); i += blockDim.x)
-        co[i] = ok ? (int64_t)src.one(i) : 0;
+      for (int e = (int)threadIdx.x; e < NCH * B; e += blockDim.x) {
+        const int lc = e / B, i = (lc * C + (int)crank) * B + e % B;
+        if (i < nc) co[i] = ok ? coefL[e] : 0;
+      }
+    }
+    __syncthreads();  // coefficients read before the next pair's state / table writes
+    if (threadIdx.x == 0 && pair + ngr < kp.batch) {  // next pair's forward-last table
+      mbar_expect(&tbar, EB * X::FLAST);
+      bulk_copy(twb + X::S_SWAP, tw + X::FWD(crank) + X::FP(4), EB * X::FLAST, &tbar);
     }
     if (crank == 0 && threadIdx.x == 0) {
       kp.cert[pair] = ok ? 1 : 0;
