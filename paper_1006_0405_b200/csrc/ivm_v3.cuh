@@ -319,7 +319,13 @@ template <typename T> struct Buf {
 // ---------------------------------------------------------------------------
 // pass 1: G_1[0][v] = x[v] (the trivial radix-2 pass 0), read from HBM;
 // G_2[2r][v] = sum_q w_R^{qr} (w_{4R}^q x[v + S'q]), stored with the mirror.
-template <typename T, int M, int RK>
+__device__ __forceinline__ unsigned ld_shared_u8(const uint8_t *p) {
+  unsigned v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)));
+  return v;
+}
+// SMEMDIG: the digits are in shared memory (staged), else global
+template <typename T, int M, int RK, bool SMEMDIG = false>
 __device__ __forceinline__ void fwd_first(const uint8_t *__restrict__ dig, int n, Buf<T> st,
                                           const TwC<T> *__restrict__ tw, int tid = threadIdx.x) {
   using Gm = G3<M, RK>;
@@ -333,7 +339,7 @@ __device__ __forceinline__ void fwd_first(const uint8_t *__restrict__ dig, int n
 #pragma unroll
       for (int q = 0; q < R; q++) {
         const int idx = nu + Sp * q;
-        const T x = idx < n ? T(dig[idx]) : T(0);
+        const T x = idx < n ? T(SMEMDIG ? ld_shared_u8(dig + idx) : (unsigned)dig[idx]) : T(0);
         if (q == 0) {
           v[g][q] = punctual(x);
         } else {
@@ -399,6 +405,7 @@ struct CertAcc {  // per-thread; reduced once per multiplication
   int ok = 1;
   int bad = 0x7fffffff;
   double rad = 0.0;
+  bool radius = true;  // track the max radius (diagnostic output only)
 };
 
 // coefficient i (global index) -> *dst (the snapped integer, or 0).  int32
@@ -412,8 +419,10 @@ __device__ __forceinline__ void certify_real(T lo, T hi, int i, int n, D *dst, C
   const double l = (double)lo, h = (double)hi;
   const double cl = ceil(l);
   const bool ok = cl == floor(h);
-  const double rad = __dmul_ru(__dadd_ru(h, -l), 0.5);
-  acc.rad = (rad <= acc.rad) ? acc.rad : rad;  // NaN propagates (comparison false)
+  if (acc.radius) {
+    const double rad = __dmul_ru(__dadd_ru(h, -l), 0.5);
+    acc.rad = (rad <= acc.rad) ? acc.rad : rad;  // NaN propagates (comparison false)
+  }
   *dst = ok ? (D)cl : (D)0;
   if (!ok) {
     acc.ok = 0;
@@ -714,8 +723,8 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
     if (staged) mbar_wait(&dbar, (unsigned)((pair - (int)blockIdx.x) / (int)gridDim.x) & 1u);
 #pragma unroll 1
     for (int op = 0; op < 2; op++) {
-      const uint8_t *dig = staged ? sdig + op * n : (op == 0 ? kp.a : kp.b) + (size_t)pair * n;
-      fwd_first<T, M, R>(dig, n, st, tw);
+      if (staged) fwd_first<T, M, R, true>(sdig + op * n, n, st, tw);
+      else fwd_first<T, M, R>((op == 0 ? kp.a : kp.b) + (size_t)pair * n, n, st, tw);
       if (op == 1 && threadIdx.x == 0) {
         cs.ok = 1;
         cs.first_bad = 0x7fffffff;
@@ -766,6 +775,7 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
       }
     }
     CertAcc acc;
+    acc.radius = kp.max_radius != nullptr;
 #pragma unroll 1
     for (int i = 0; i < NINV; i++) {
       const PassRT pp = pick_inv<M, R>(i);
