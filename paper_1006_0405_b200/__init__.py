@@ -46,30 +46,33 @@ def lib():
                               "(there is no fallback implementation)")
         L = ctypes.CDLL(LIB_PATH)
         P, S, I, U64 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_uint64
-        L.ivm_version.restype = ctypes.c_char_p
-        L.ivm_strerror.restype = ctypes.c_char_p
-        L.ivm_strerror.argtypes = [I]
-        L.ivm_max_digits.restype = S
-        L.ivm_max_digits.argtypes = [I]
-        L.ivm_fft_length.restype = S
-        L.ivm_fft_length.argtypes = [S]
-        L.ivm_create.argtypes = [ctypes.POINTER(P), I]
-        L.ivm_destroy.argtypes = [P]
-        L.ivm_reserve.argtypes = [P, S, S, I]
-        L.ivm_multiply.argtypes = [P, P, P, S, P, P, I, P]
-        L.ivm_multiply_batched.argtypes = [P, P, P, S, S, P, P, I, P]
-        L.ivm_multiply_batched_diag.argtypes = [P, P, P, S, S, P, P, I, P, P, P, P, P, S, P]
-        L.ivm_multiply_batched_host.argtypes = [P, P, P, S, S, P, P, I, P]
-        L.ivm_generate_digits.argtypes = [P, P, S, S, U64, U64, I, I, P, P]
-        L.ivm_peak_probe.argtypes = [P, I, I, P, ctypes.POINTER(U64), P]
-        L.ivm_last_launch_count.argtypes = [P]
-        L.ivm_twiddle_table.argtypes = [I, I, P]
-        L.ivm_long_multiply_batched.argtypes = [P, P, P, S, S, P, P]
-        L.ivm_multiply_exact.argtypes = [P, P, P, S, S, P, P, I, P]
-        L.ivm_multiply_naive.argtypes = [P, P, P, S, S, P, I, P]
-        L.ivm_multi_create.argtypes = [ctypes.POINTER(P), I, P]
-        L.ivm_multi_multiply.argtypes = [P, P, P, S, S, P, P, I, I, P, P]
-        L.ivm_multi_destroy.argtypes = [P]
+        sig = {
+            "ivm_version": (None, ctypes.c_char_p), "ivm_strerror": ([I], ctypes.c_char_p),
+            "ivm_max_digits": ([I], S), "ivm_fft_length": ([S], S),
+            "ivm_create": ([ctypes.POINTER(P), I], None), "ivm_destroy": ([P], None),
+            "ivm_reserve": ([P, S, S, I], None), "ivm_multiply": ([P, P, P, S, P, P, I, P], None),
+            "ivm_multiply_batched": ([P, P, P, S, S, P, P, I, P], None),
+            "ivm_multiply_batched_diag": ([P, P, P, S, S, P, P, I, P, P, P, P, P, S, P], None),
+            "ivm_multiply_batched_host": ([P, P, P, S, S, P, P, I, P], None),
+            "ivm_generate_digits": ([P, P, S, S, U64, U64, I, I, P, P], None),
+            "ivm_peak_probe": ([P, I, I, P, ctypes.POINTER(U64), P], None),
+            "ivm_last_launch_count": ([P], None), "ivm_twiddle_table": ([I, I, P], None),
+            "ivm_long_multiply_batched": ([P, P, P, S, S, P, P], None),
+            "ivm_multiply_exact": ([P, P, P, S, S, P, P, I, P], None),
+            "ivm_multiply_naive": ([P, P, P, S, S, P, I, P], None),
+            "ivm_multi_create": ([ctypes.POINTER(P), I, P], None),
+            "ivm_multi_multiply": ([P, P, P, S, S, P, P, I, I, P, P], None),
+            "ivm_multi_destroy": ([P], None),
+        }
+        # (an older build missing a symbol fails at that call, not at load:
+        # tests/test_abi.py checks that this build exports every declared one)
+        for name, (args, res) in sig.items():
+            if hasattr(L, name):
+                f = getattr(L, name)
+                if args is not None:
+                    f.argtypes = args
+                if res is not None:
+                    f.restype = res
         _lib = L
     return _lib
 

@@ -577,7 +577,11 @@ int ivm_multiply_batched_host(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, s
   }
   // chunks of whole waves (multiples of the SM count), at most kChunks: the
   // copy-in of chunk i+1 and the copy-out of chunk i-1 overlap the kernel of chunk i
-  const int kChunks = 8;
+  static const int kChunks = [] {  // IVM_HOST_CHUNKS overrides (tuning)
+    const char *e = getenv("IVM_HOST_CHUNKS");
+    const int v = e ? atoi(e) : 0;
+    return v >= 1 && v <= 64 ? v : 8;
+  }();
   const size_t sms = (size_t)(c->sms > 0 ? c->sms : 1);
   size_t chunk = batch;
   if (batch >= 2 * sms) {
@@ -597,13 +601,19 @@ int ivm_multiply_batched_host(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, s
   if (cudaEventRecord(e0, s) != cudaSuccess || cudaStreamWaitEvent(c->s_in, e0, 0) != cudaSuccess)
     return cuda_fail(c);
   int launches = 0;
+  // all copy-ins first: a copy-out waiting on its kernel must not sit ahead of
+  // a later copy-in in a shared copy queue
+  for (size_t k = 0; k < nchunks; k++) {
+    const size_t p0 = k * chunk, bk = (batch - p0 < chunk) ? batch - p0 : chunk;
+    if (cudaMemcpyAsync(da + p0 * n, a + p0 * n, bk * n, cudaMemcpyHostToDevice, c->s_in) != cudaSuccess ||
+        cudaMemcpyAsync(db + p0 * n, b + p0 * n, bk * n, cudaMemcpyHostToDevice, c->s_in) != cudaSuccess ||
+        cudaEventRecord(c->ev[3 * k], c->s_in) != cudaSuccess)
+      return cuda_fail(c);
+  }
   for (size_t k = 0; k < nchunks; k++) {
     const size_t p0 = k * chunk, bk = (batch - p0 < chunk) ? batch - p0 : chunk;
     cudaEvent_t e_in = c->ev[3 * k], e_run = c->ev[3 * k + 1], e_out = c->ev[3 * k + 2];
-    if (cudaMemcpyAsync(da + p0 * n, a + p0 * n, bk * n, cudaMemcpyHostToDevice, c->s_in) != cudaSuccess ||
-        cudaMemcpyAsync(db + p0 * n, b + p0 * n, bk * n, cudaMemcpyHostToDevice, c->s_in) != cudaSuccess ||
-        cudaEventRecord(e_in, c->s_in) != cudaSuccess || cudaStreamWaitEvent(s, e_in, 0) != cudaSuccess)
-      return cuda_fail(c);
+    if (cudaStreamWaitEvent(s, e_in, 0) != cudaSuccess) return cuda_fail(c);
     r = ivm_multiply_batched(c, da + p0 * n, db + p0 * n, n, bk, dp + p0 * 2 * n, dc + p0, prec, stream);
     if (r) return r;
     launches += c->last_launches;
