@@ -232,3 +232,27 @@ def test_argument_errors(ctx):
     assert L.ivm_multiply_batched(ctx._h, p, p, 4, 1, p, p, 5, None) == -1   # precision
     big = ivm.max_digits(ivm.F64) + 1
     assert L.ivm_multiply_batched(ctx._h, p, p, big, 1, p, p, 0, None) == -4
+
+
+@pytest.mark.parametrize("n", [1024, 4096, 16384])
+def test_misaligned_operands_and_products(ctx, n):
+    """Operand / product pointers at odd byte offsets: the digit staging (TMA,
+    16-B aligned rows only) and the 4-byte digit stores take their fallbacks;
+    results identical to the aligned call."""
+    import torch
+    B = 6
+    a, b = inputs.pair_digits(0x0DD + n, np.arange(B), n, np.array([0, 1, 2, 3, 0, 1]))
+    ta = torch.zeros(B * n + 3, dtype=torch.uint8, device="cuda")
+    tb = torch.zeros(B * n + 5, dtype=torch.uint8, device="cuda")
+    ta[3:] = torch.from_numpy(a.reshape(-1)).cuda()
+    tb[5:] = torch.from_numpy(b.reshape(-1)).cuda()
+    va, vb = ta[3:].view(B, n), tb[5:].view(B, n)
+    po = torch.zeros(B * 2 * n + 7, dtype=torch.uint8, device="cuda")
+    pc = torch.zeros(B + 1, dtype=torch.uint8, device="cuda")
+    out, cert = ctx.multiply(va, vb, out=po[7:].view(B, 2 * n), cert=pc[1:])
+    torch.cuda.synchronize()
+    assert cert.cpu().numpy().all()
+    big = lambda d: int.from_bytes(bytes(d), "little")
+    o = out.cpu().numpy()
+    for p in range(B):
+        assert big(o[p]) == big(a[p]) * big(b[p]), p
