@@ -50,9 +50,9 @@ def W_ops(m: int) -> int:
     return 24 * m * L - 28 * m + 48
 
 
-def load_traffic(config: str):
-    """DRAM bytes per launch of the dominant kernel from the committed ncu
-    --set full capture of this config (latest round under profiles/), else None."""
+def load_profile(config: str):
+    """The committed ncu record of this config's dominant kernel (latest round
+    under profiles/), else None."""
     try:
         rounds = sorted(d for d in os.listdir(os.path.join(ROOT, "profiles")) if d.startswith("r"))
         for r in reversed(rounds):
@@ -60,10 +60,16 @@ def load_traffic(config: str):
             if os.path.exists(f):
                 t = json.load(open(f)).get(config)
                 if t:
-                    return t["dram_bytes_per_launch"]
+                    return dict(t, file=f"profiles/{r}/ncu_traffic.json")
     except Exception:
         pass
     return None
+
+
+def load_traffic(config: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture."""
+    t = load_profile(config)
+    return t["dram_bytes_per_launch"] if t else None
 
 
 def load_peaks():
@@ -336,6 +342,12 @@ def run_ours(args):
                          "unit": "Top/s (directed FP64 DADD/DMUL/DFMA, FMA = 1 op)",
                          "frac": achieved / peak_ops, "traffic": load_traffic(args.config),
                          "traffic_unit": "DRAM bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
+                         "hw_counters": ({k: load_profile(args.config)[k] for k in
+                                          ("kernel", "fp64_pipe_active_pct", "issue_active_pct", "file")
+                                          if k in load_profile(args.config)}
+                                         if load_profile(args.config) else None),
+                         "note": "W credits the paper's full complex FFT; the half-spectrum kernels execute about "
+                                 "0.5 W FP64 instructions, so the FP64 pipe is busier than frac only by that factor",
                          "work_per_unit": f"W(m) = 24 m log2 m - 28 m + 48 = {W_ops(m)} ops per multiplication (SURVEY.md 8(d.1))",
                          "peak_basis": f"148 SM x 64 FP64 lanes x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz); directed-DFMA probe measured {probe/1e12 if probe else float('nan'):.2f} Top/s",
                          "kernel_ms": ms_per_step},
