@@ -347,7 +347,7 @@ def run_ours(args):
                                           if k in load_profile(args.config)}
                                          if load_profile(args.config) else None),
                          "note": "W credits the paper's full complex FFT; the half-spectrum kernels execute about "
-                                 "0.5 W FP64 instructions, so the FP64 pipe is busier than frac only by that factor",
+                                 "0.5 W FP64 instructions, so the hardware FP64 pipe is about half as busy as frac (hw_counters)",
                          "work_per_unit": f"W(m) = 24 m log2 m - 28 m + 48 = {W_ops(m)} ops per multiplication (SURVEY.md 8(d.1))",
                          "peak_basis": f"148 SM x 64 FP64 lanes x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz); directed-DFMA probe measured {probe/1e12 if probe else float('nan'):.2f} Top/s",
                          "kernel_ms": ms_per_step},
