@@ -66,6 +66,21 @@ def load_profile(config: str):
     return None
 
 
+def load_counters(config: str):
+    """SURVEY §8(d.4) ncu counters of this config's dominant kernel (committed)."""
+    try:
+        rounds = sorted(d for d in os.listdir(os.path.join(ROOT, "profiles")) if d.startswith("r"))
+        for r in reversed(rounds):
+            f = os.path.join(ROOT, "profiles", r, "ncu_counters.json")
+            if os.path.exists(f):
+                t = json.load(open(f)).get(config)
+                if t:
+                    return dict(t, file=f"profiles/{r}/ncu_counters.json")
+    except Exception:
+        pass
+    return None
+
+
 def load_traffic(config: str):
     """DRAM bytes per launch of the dominant kernel from the committed ncu capture."""
     t = load_profile(config)
@@ -147,6 +162,16 @@ class ClockSampler:
                 "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(a, b, n, prec, budget_s=12.0):
     """The oracle as it stands (oracle/, plain C, OpenMP over pairs) on the host
     cores, on a bounded sample of the same workload."""
@@ -166,7 +191,7 @@ def cpu_baseline(a, b, n, prec, budget_s=12.0):
         dt = time.perf_counter() - t0
         k = k2
     certified = int(np.asarray(r["cert"]).sum())
-    return {"value": certified * n / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+    return {"value": certified * n / dt, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu": cpu_model(),
             "sample": f"first {k} of {B} pairs of the same workload ({certified} certified), {dt:.2f} s wall"}
 
 
@@ -201,7 +226,7 @@ def run_reference(args):
             "impl": "reference",
             "config": {"workload": text, "n": n, "batch": batch, "fft_length": 1 << math.ceil(math.log2(2 * n - 1)),
                        "step_sample": f"{k} pairs per step (bounded sample of the {batch}-pair batch)"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu": cpu_model(),
                              "sample": f"{k} of {batch} pairs per step"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -342,10 +367,13 @@ def run_ours(args):
                          "unit": "Top/s (directed FP64 DADD/DMUL/DFMA, FMA = 1 op)",
                          "frac": achieved / peak_ops, "traffic": load_traffic(args.config),
                          "traffic_unit": "DRAM bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
-                         "hw_counters": ({k: load_profile(args.config)[k] for k in
-                                          ("kernel", "fp64_pipe_active_pct", "issue_active_pct", "file")
-                                          if k in load_profile(args.config)}
-                                         if load_profile(args.config) else None),
+                         "hw_counters": ({k: load_counters(args.config)[k] for k in
+                                          ("kernel", "executed_fp64_thread_ops_per_mult", "credited_W_per_mult",
+                                           "executed_over_W", "fp64_pipe_active_pct", "issue_active_pct",
+                                           "dram_bytes", "registers_per_thread", "warps_active_pct", "file")
+                                          if k in load_counters(args.config)}
+                                         if load_counters(args.config) else None),
+                         "frac_vs_probe": (achieved / probe) if probe else None,
                          "note": "W credits the paper's full complex FFT; the half-spectrum kernels execute about "
                                  "0.5 W FP64 instructions, so the hardware FP64 pipe is about half as busy as frac (hw_counters)",
                          "work_per_unit": f"W(m) = 24 m log2 m - 28 m + 48 = {W_ops(m)} ops per multiplication (SURVEY.md 8(d.1))",
