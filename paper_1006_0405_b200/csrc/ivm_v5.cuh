@@ -320,15 +320,35 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
       link[crank * 8 + 3] = (unsigned)(cs.maxrad >> 32);
     }
     gsync(ctr, C, gen);  // (2) certificates and chunk boundaries of every CTA visible
-    int ok = 1, bad = 0x7fffffff;
-    unsigned long long rad = 0ull;
-    for (int p = 0; p < C; p++) {
-      const volatile unsigned *lp = link + p * 8;
-      ok &= (int)lp[0];
-      bad = min(bad, (int)lp[1]);
-      const unsigned long long rp = (unsigned long long)lp[2] | ((unsigned long long)lp[3] << 32);
-      rad = rp > rad ? rp : rad;
+    // the group's certificate: one warp reads the C link records (L2) and broadcasts
+    __shared__ int s_ok, s_bad;
+    __shared__ unsigned long long s_rad;
+    if (threadIdx.x < 32) {
+      const unsigned l = threadIdx.x;
+      int okl = 1, badl = 0x7fffffff;
+      unsigned long long radl = 0ull;
+      if ((int)l < C) {
+        const uint4 w = __ldcg(reinterpret_cast<const uint4 *>(link + l * 8));
+        okl = (int)w.x;
+        badl = (int)w.y;
+        radl = (unsigned long long)w.z | ((unsigned long long)w.w << 32);
+      }
+      okl = __reduce_and_sync(0xffffffffu, (unsigned)okl);
+      badl = (int)__reduce_min_sync(0xffffffffu, (unsigned)badl);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const unsigned long long r2 = __shfl_xor_sync(0xffffffffu, radl, o);
+        radl = r2 > radl ? r2 : radl;
+      }
+      if (l == 0) {
+        s_ok = okl;
+        s_bad = badl;
+        s_rad = radl;
+      }
     }
+    __syncthreads();
+    const int ok = s_ok, bad = s_bad;
+    const unsigned long long rad = s_rad;
     const int words = (nout + 3) / 4, warp = (int)threadIdx.x >> 5;
     uint8_t *out = kp.prod + (size_t)pair * nout;
     __shared__ uint8_t s_cin[64];
