@@ -375,15 +375,34 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
       bulk_copy(twb + X::S_SWAP, tw + X::FWD(crank) + X::FP(4), EB * X::FLAST, &tbar);
     }
     cluster_sync();  // (3) coefficients and per-CTA certificates complete
-    int ok = 1, bad = 0x7fffffff;
-    unsigned long long rad = 0ull;
+    // the C per-CTA certificates: lane p of warp 0 reads CTA p's, the warp
+    // reduces, shared memory broadcasts (one remote read per CTA, not per thread)
+    __shared__ int s_ok, s_bad;
+    __shared__ unsigned long long s_rad;
+    if (threadIdx.x < 32) {
+      int okl = 1, badl = 0x7fffffff;
+      unsigned long long radl = 0ull;
+      if ((int)threadIdx.x < C) {
+        okl = dsm_ld_i32(dsm_map(&cs.ok, threadIdx.x));
+        badl = dsm_ld_i32(dsm_map(&cs.first_bad, threadIdx.x));
+        radl = dsm_ld_u64(dsm_map(&cs.maxrad, threadIdx.x));
+      }
+      okl = (int)__reduce_and_sync(0xffffffffu, (unsigned)okl);
+      badl = __reduce_min_sync(0xffffffffu, badl);
 #pragma unroll
-    for (int p = 0; p < C; p++) {
-      ok &= dsm_ld_i32(dsm_map(&cs.ok, (unsigned)p));
-      bad = min(bad, dsm_ld_i32(dsm_map(&cs.first_bad, (unsigned)p)));
-      const unsigned long long rp = dsm_ld_u64(dsm_map(&cs.maxrad, (unsigned)p));
-      rad = rp > rad ? rp : rad;
+      for (int o = 16; o; o >>= 1) {
+        const unsigned long long r2 = __shfl_xor_sync(0xffffffffu, radl, o);
+        radl = r2 > radl ? r2 : radl;
+      }
+      if (threadIdx.x == 0) {
+        s_ok = okl;
+        s_bad = badl;
+        s_rad = radl;
+      }
     }
+    __syncthreads();
+    const int ok = s_ok, bad = s_bad;
+    const unsigned long long rad = s_rad;
     // carry: coefficient chunk ch (B coefficients, B/4 words) lives in CTA ch mod C
     // at local chunk ch / C, so each CTA carries its own 2C chunks, one team of
     // 8/C warps per chunk; only the chunks' (generate, all-propagate) bits and
