@@ -25,6 +25,7 @@ struct ivm_ctx {
   std::map<std::pair<int, int>, ivm::LaunchInfo> info;
   std::map<std::pair<int, int>, ivm::LaunchInfo> info3;
   bool force_v1 = false;
+  bool force_v5 = false;   // IVM_KERNEL=v5: the group kernel also for m = 2^14 .. 2^16
   bool force_v3g = false;  // IVM_KERNEL=v3g: the older global-state group kernel for every m >= 2^14
   std::map<std::pair<int, int>, void *> tw4;  // (log2m, prec) -> v4 role tables
   std::map<std::pair<int, int>, ivm::LaunchInfo> info4;
@@ -128,6 +129,7 @@ int ivm_create(ivm_ctx_t *ctx, int device) {
   const char *kv = getenv("IVM_KERNEL");
   c->force_v1 = kv && strcmp(kv, "v1") == 0;
   c->force_v3g = kv && strcmp(kv, "v3g") == 0;
+  c->force_v5 = kv && strcmp(kv, "v5") == 0;
   c->consts = true;
   *ctx = c;
   return IVM_OK;
@@ -178,8 +180,8 @@ static bool use_v3(ivm_ctx_t c, int m) { return !c->force_v1 && m >= 10 && m <= 
 // fp64 only: at fp32 (C4, the precision-limit sweep) the v1 kernel's full-interval
 // twiddles give ~2x tighter enclosures (93 % vs 0 % of 32-digit uniform pairs certified)
 static bool use_v6(ivm_ctx_t c, int m, int prec) { return !c->force_v1 && prec == IVM_F64 && m >= 6 && m <= 9; }
-static bool use_v4(ivm_ctx_t c, int m) { return !c->force_v3g && m >= 14 && m <= 16; }
-static bool use_v5(ivm_ctx_t c, int m) { return !c->force_v3g && (m == 17 || m == 18); }
+static bool use_v4(ivm_ctx_t c, int m) { return !c->force_v3g && !c->force_v5 && m >= 14 && m <= 16; }
+static bool use_v5(ivm_ctx_t c, int m) { return !c->force_v3g && m >= 14 && m <= 18 && !use_v4(c, m); }
 static bool use_v3g(ivm_ctx_t c, int m) { return m >= 14 && m <= 18 && !use_v4(c, m) && !use_v5(c, m); }
 
 static int get_info5(ivm_ctx_t c, int m, int prec, ivm::LaunchInfo *li) {

@@ -1,4 +1,4 @@
-// ivm_v5.cu -- translation unit of the group kernel for m = 2^17, 2^18
+// ivm_v5.cu -- translation unit of the group kernel for m = 2^14 .. 2^18
 // (ivm_v5.cuh): launch info and the cooperative launch.  Its twiddle tables are
 // the v4 layout (v4_tables, ivm_v4.cu).
 #include <cuda_runtime.h>
@@ -47,6 +47,9 @@ template <typename T, int M> static int v5_info_impl(LaunchInfo *li) {
 }
 #define IVM_V5_DISPATCH(FN, ...)         \
   switch (m) {                           \
+    case 14: return FN<14>(__VA_ARGS__); \
+    case 15: return FN<15>(__VA_ARGS__); \
+    case 16: return FN<16>(__VA_ARGS__); \
     case 17: return FN<17>(__VA_ARGS__); \
     case 18: return FN<18>(__VA_ARGS__); \
     default: return -4;                  \

@@ -1,23 +1,26 @@
-// ivm_v5.cuh -- group kernel for m = 2^17, 2^18 (C = 16, 32 CTAs per
-// multiplication; included by ivm_v5.cu).
+// ivm_v5.cuh -- group kernel for m = 2^14 .. 2^18 (C = 2 .. 32 CTAs per
+// multiplication; included by ivm_v5.cu).  The default route for m = 2^17, 2^18
+// (too large for a thread-block cluster); for C <= 8 it is the alternative to
+// the cluster kernel that packs onto every SM (clusters of 4 and 8 CTAs must fit
+// a GPC, which strands SMs).
 //
 // The same row split and local m = 8192 schedule as the cluster kernel
-// (ivm_v4.cuh), for groups too large for a thread-block cluster: the C CTAs of
-// a group are co-resident (cooperative launch) and exchange through L2-resident
-// global scratch with group barriers (global atomics) instead of DSMEM.
+// (ivm_v4.cuh), with the C CTAs of a group co-resident (cooperative launch) and
+// exchanging through L2-resident global scratch with group barriers (global
+// atomics) instead of DSMEM.
 //   * after the local inverse passes 0..3 every CTA writes its column of the
 //     4096 inverse rows to scratch; barrier;
 //   * CTA c gathers rows [c B, c B + B) of all C columns and runs the last
-//     inverse pass (radix C, untwist folded into the input twiddles) as two
-//     shared-memory stages, C = 8 C2:
+//     inverse pass (radix C, untwist folded into the input twiddles): for
+//     C <= 8 in registers, for C = 8 C2 > 8 as two shared-memory stages
 //       out_{r1 + 8 r2} = sum_b w_{C2}^{-b r2} [ w_C^{-b r1} sum_a w_8^{-a r1} y_{C2 a + b} ],
 //     then scales, certifies and snaps c_k, c_{k+m/2} (k = k0 + 4096 r) into
-//     its own shared memory (int64: 255^2 n > 2^31 here): chunk ch of B
+//     its own shared memory (int64: 255^2 n > 2^31 at m >= 2^17): chunk ch of B
 //     consecutive coefficients lives in CTA ch mod C; every CTA publishes its
 //     chunks' last 8 coefficients; barrier;
-//   * each CTA carries its own chunks (one warp per chunk) and publishes their
-//     generate / all-propagate bits; barrier; the carries into all 2 C^2 chunks
-//     follow from one ballot adder; digits out.
+//   * each CTA carries its own 2C chunks (a team of max(1, 8/C) warps per chunk)
+//     and publishes their generate / all-propagate bits; barrier; the carries
+//     into all 2 C^2 chunks follow from one ballot adder; digits out.
 #pragma once
 
 namespace ivm {
@@ -96,6 +99,7 @@ template <typename T, int M> struct Cfg5 {
   static constexpr size_t SMEM = STATE_BYTES + TW_BYTES;
   static constexpr size_t A_BYTES = 2 * E * 4096;
   static_assert(SMEM <= 227 * 1024, "shared memory");
+  static_assert(STATE_BYTES >= 8 * 8192, "int64 coefficients fit the state");
 };
 
 // c = 2 Re / m, 2 Im / m of t = w o (w: full interval), certified into d0, d1
@@ -115,7 +119,9 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
   using GL = G3<13, 8>;
   using CF = Cfg5<T, M>;
   using V = typename V2t<T>::t;
-  constexpr int C = X::C, B = X::B, C2 = C / 8, R = 8, NL = 8192, N = 1 << M;
+  constexpr int C = X::C, B = X::B, R = 8, NL = 8192, N = 1 << M;
+  constexpr bool TWO = C > 8;  // two-stage last inverse pass
+  constexpr int C2 = TWO ? C / 8 : 1;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Cert3 cs;
   __shared__ CarrySeg seg;
@@ -231,74 +237,100 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
     }
     gsync(ctr, C, gen);  // (1) all columns written
     mbar_wait(&tbar, par);
-    // gather + input twiddles: y_q(kl) -> state[q B + kl]
-#pragma unroll
-    for (int j = 0; j < 8; j++) {
-      const int idx = (int)threadIdx.x + 512 * j, q = idx / B, kl = idx % B;
-      const int src = (2 * q < C) ? 2 * q : 2 * C - 1 - 2 * q;
-      CI<T> z = ldcg_ci(xch + (size_t)src * 4096 + (int)crank * B + kl);
-      const TwC<T> w = twb[X::S_SWAP + q * B + kl];
-      z = (2 * q < C) ? rtmul<T, true, true>(w, z) : rtmul<T, false, true>(w, cconj(z));
-      st.st(idx, z);
-    }
-    __syncthreads();
-    {  // stage 1: task (b, kl), DFT8 over a, times w_C^{-b r1}
-      const int b = (int)threadIdx.x / B, kl = (int)threadIdx.x % B;
-      CI<T> v[8];
-#pragma unroll
-      for (int a = 0; a < 8; a++) v[a] = st.ld((C2 * a + b) * B + kl);
-      cdft<T, 8, true>(v);
-#pragma unroll
-      for (int r1 = 1; r1 < 8; r1++) v[r1] = cmul(s2tw[b * r1], v[r1]);
-      __syncthreads();
-#pragma unroll
-      for (int r1 = 0; r1 < 8; r1++) st.st((r1 * C2 + b) * B + kl, v[r1]);
-      __syncthreads();
-    }
     CertAcc acc;
-    // stage 2: task (r1, kl), DFT_C2 over b, untwist remainder, emit.  The
-    // coefficients go to this CTA's shared memory (int64), chunk ch = (h C + r)
-    // of B consecutive c_i: fp64 into the twiddle swap buffer (free until the
-    // next pair's forward-last table, fetched after the carry), fp32 (whose swap
-    // buffer is too small) into the state once every input is in registers
-    constexpr int TASKS = 8 * B / 512;
-    constexpr bool IN_SWAP = sizeof(TwC<T>) * 4096 >= 8 * 8192;
+    // the coefficients (int64): fp64 two-stage into the twiddle swap buffer (free
+    // until the next pair's forward-last table, fetched after the carry), else
+    // into the state (free once every input is in registers)
+    constexpr bool IN_SWAP = TWO && sizeof(TwC<T>) * 4096 >= 8 * 8192;
     long long *coefL = IN_SWAP ? reinterpret_cast<long long *>(twb + X::S_SWAP) : reinterpret_cast<long long *>(smem);
-    {
+    if constexpr (!TWO) {  // radix C <= 8 in registers: task (g, kl), rows crank B + kl + 512 g
+      constexpr int G = 8 / C;
+      CI<T> v[G][C];
+#pragma unroll
+      for (int g = 0; g < G; g++) {
+        const int kl = (int)threadIdx.x + 512 * g;
+#pragma unroll
+        for (int q = 0; q < C; q++) {
+          const int src = (2 * q < C) ? 2 * q : 2 * C - 1 - 2 * q;
+          const CI<T> z = ldcg_ci(xch + (size_t)src * 4096 + (int)crank * B + kl);
+          const TwC<T> w = twb[X::S_SWAP + q * B + kl];
+          v[g][q] = (2 * q < C) ? rtmul<T, true, true>(w, z) : rtmul<T, false, true>(w, cconj(z));
+        }
+        cdft<T, C, true>(v[g]);
+      }
       double *dump = diag_dump(kp, pair, N);
-      if constexpr (IN_SWAP) {
 #pragma unroll
-        for (int g2 = 0; g2 < TASKS; g2++) {
-          const int task = (int)threadIdx.x + 512 * g2, r1 = task / B, kl = task % B;
-          const int k0 = (int)crank * B + kl;
-          CI<T> v[C2];
+      for (int g = 0; g < G; g++) {
+        const int kl = (int)threadIdx.x + 512 * g, k0 = (int)crank * B + kl;
 #pragma unroll
-          for (int b = 0; b < C2; b++) v[b] = st.ld((r1 * C2 + b) * B + kl);
-          cdft<T, C2, true>(v);
+        for (int r = 0; r < C; r++)
+          emit_tab<T, M>(v[g][r], fold[r], k0 + 4096 * r, n, coefL + r * B + kl, coefL + (C + r) * B + kl, acc, dump);
+      }
+    } else {
+      // gather + input twiddles: y_q(kl) -> state[q B + kl]
 #pragma unroll
-          for (int r2 = 0; r2 < C2; r2++) {
-            const int r = r1 + 8 * r2, k = k0 + 4096 * r;
-            emit_tab<T, M>(v[r2], fold[r], k, n, coefL + r * B + kl, coefL + (C + r) * B + kl, acc, dump);
+      for (int j = 0; j < 8; j++) {
+        const int idx = (int)threadIdx.x + 512 * j, q = idx / B, kl = idx % B;
+        const int src = (2 * q < C) ? 2 * q : 2 * C - 1 - 2 * q;
+        CI<T> z = ldcg_ci(xch + (size_t)src * 4096 + (int)crank * B + kl);
+        const TwC<T> w = twb[X::S_SWAP + q * B + kl];
+        z = (2 * q < C) ? rtmul<T, true, true>(w, z) : rtmul<T, false, true>(w, cconj(z));
+        st.st(idx, z);
+      }
+      __syncthreads();
+      {  // stage 1: task (b, kl), DFT8 over a, times w_C^{-b r1}
+        const int b = (int)threadIdx.x / B, kl = (int)threadIdx.x % B;
+        CI<T> v[8];
+#pragma unroll
+        for (int a = 0; a < 8; a++) v[a] = st.ld((C2 * a + b) * B + kl);
+        cdft<T, 8, true>(v);
+#pragma unroll
+        for (int r1 = 1; r1 < 8; r1++) v[r1] = cmul(s2tw[b * r1], v[r1]);
+        __syncthreads();
+#pragma unroll
+        for (int r1 = 0; r1 < 8; r1++) st.st((r1 * C2 + b) * B + kl, v[r1]);
+        __syncthreads();
+      }
+      // stage 2: task (r1, kl), DFT_C2 over b, untwist remainder, emit; chunk
+      // ch = (h C + r) of B consecutive c_i (fp32, whose swap buffer is too
+      // small, waits until every input is in registers)
+      constexpr int TASKS = 8 * B / 512;
+      {
+        double *dump = diag_dump(kp, pair, N);
+        if constexpr (IN_SWAP) {
+#pragma unroll
+          for (int g2 = 0; g2 < TASKS; g2++) {
+            const int task = (int)threadIdx.x + 512 * g2, r1 = task / B, kl = task % B;
+            const int k0 = (int)crank * B + kl;
+            CI<T> v[C2];
+#pragma unroll
+            for (int b = 0; b < C2; b++) v[b] = st.ld((r1 * C2 + b) * B + kl);
+            cdft<T, C2, true>(v);
+#pragma unroll
+            for (int r2 = 0; r2 < C2; r2++) {
+              const int r = r1 + 8 * r2, k = k0 + 4096 * r;
+              emit_tab<T, M>(v[r2], fold[r], k, n, coefL + r * B + kl, coefL + (C + r) * B + kl, acc, dump);
+            }
           }
-        }
-      } else {
-        CI<T> v[TASKS][C2];
+        } else {
+          CI<T> v[TASKS][C2];
 #pragma unroll
-        for (int g2 = 0; g2 < TASKS; g2++) {
-          const int task = (int)threadIdx.x + 512 * g2, r1 = task / B, kl = task % B;
+          for (int g2 = 0; g2 < TASKS; g2++) {
+            const int task = (int)threadIdx.x + 512 * g2, r1 = task / B, kl = task % B;
 #pragma unroll
-          for (int b = 0; b < C2; b++) v[g2][b] = st.ld((r1 * C2 + b) * B + kl);
-        }
-        __syncthreads();  // the state is free for the coefficients
+            for (int b = 0; b < C2; b++) v[g2][b] = st.ld((r1 * C2 + b) * B + kl);
+          }
+          __syncthreads();  // the state is free for the coefficients
 #pragma unroll
-        for (int g2 = 0; g2 < TASKS; g2++) {
-          const int task = (int)threadIdx.x + 512 * g2, r1 = task / B, kl = task % B;
-          const int k0 = (int)crank * B + kl;
-          cdft<T, C2, true>(v[g2]);
+          for (int g2 = 0; g2 < TASKS; g2++) {
+            const int task = (int)threadIdx.x + 512 * g2, r1 = task / B, kl = task % B;
+            const int k0 = (int)crank * B + kl;
+            cdft<T, C2, true>(v[g2]);
 #pragma unroll
-          for (int r2 = 0; r2 < C2; r2++) {
-            const int r = r1 + 8 * r2, k = k0 + 4096 * r;
-            emit_tab<T, M>(v[g2][r2], fold[r], k, n, coefL + r * B + kl, coefL + (C + r) * B + kl, acc, dump);
+            for (int r2 = 0; r2 < C2; r2++) {
+              const int r = r1 + 8 * r2, k = k0 + 4096 * r;
+              emit_tab<T, M>(v[g2][r2], fold[r], k, n, coefL + r * B + kl, coefL + (C + r) * B + kl, acc, dump);
+            }
           }
         }
       }
@@ -306,7 +338,10 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
     cert_flush(acc, cs);
     __syncthreads();
     // chunk ch (global, B coefficients from ch B) is local chunk lc = ch / C of CTA ch % C
-    constexpr int NCH = 2 * C, NCHT = 2 * C * C, WB = B / 4, ROUNDS = NCH / 16;
+    // teams: one warp per chunk and NCH / 16 rounds (C >= 8), else one round of
+    // 16 / NCH warps per chunk
+    constexpr int NCH = 2 * C, NCHT = 2 * C * C, WB = B / 4;
+    constexpr int TWP = NCH >= 16 ? 1 : 16 / NCH, ROUNDS = NCH >= 16 ? NCH / 16 : 1;
     long long *bnd = g.bnd + (size_t)gi * NCHT * 8;
     uint8_t *bits = g.bits + (size_t)gi * NCHT;
     for (int e = (int)threadIdx.x; e < NCH * 8; e += blockDim.x) {  // boundary words of the own chunks
@@ -358,33 +393,43 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
       s_prev[lc][e % 8] = ch > 0 ? __ldcg(bnd + (size_t)(ch - 1) * 8 + e % 8) : 0ll;
     }
     __syncthreads();
-    // scan: one warp per chunk, ROUNDS chunks per warp
+    const int w0 = warp / TWP * TWP;  // first warp of this thread's team
 #pragma unroll 1
     for (int rd = 0; rd < ROUNDS; rd++) {
-      const int lc = rd * 16 + warp, ch = lc * C + (int)crank;
+      const int lc = rd * 16 + warp / TWP, ch = lc * C + (int)crank;
       const int kb = min(ch * WB, words), ke = min(kb + WB, words);
       const ChunkSrc src{coefL + lc * B, s_prev[lc], ch * B};
       unsigned gn = 0u, ap = 1u;
-      if (ok) carry_seg_scan(src, nc, kb, ke, seg, gn, ap, warp, 1);
-      if ((threadIdx.x & 31) == 0) bits[ch] = (uint8_t)(gn | (ap << 1));
+      if (ok) carry_seg_scan(src, nc, kb, ke, seg, gn, ap, w0, TWP);
+      if ((int)threadIdx.x == 32 * w0) bits[ch] = (uint8_t)(gn | (ap << 1));
     }
     gsync(ctr, C, gen);  // (3) every chunk's generate / all-propagate visible
     if (ok) {
       if (threadIdx.x < 32) {  // carries into all 2C^2 chunks: 64 chunks per lane, then across lanes
         const int l = (int)threadIdx.x;
         unsigned long long G = 0ull, P = ~0ull;  // beyond the chunks: propagate
-        if (64 * l < NCHT) {  // NCHT is a multiple of 64: 4 x 16 B per lane
-          P = 0ull;
-          const uint4 *bp = reinterpret_cast<const uint4 *>(bits + 64 * l);
+        if (64 * l < NCHT) {
+          if constexpr (NCHT % 64 == 0) {  // 4 x 16 B per lane
+            P = 0ull;
+            const uint4 *bp = reinterpret_cast<const uint4 *>(bits + 64 * l);
 #pragma unroll
-          for (int q = 0; q < 4; q++) {
-            const uint4 w = __ldcg(bp + q);
-            const unsigned ws[4] = {w.x, w.y, w.z, w.w};
+            for (int q = 0; q < 4; q++) {
+              const uint4 w = __ldcg(bp + q);
+              const unsigned ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-            for (int e = 0; e < 16; e++) {
-              const unsigned bb = (ws[e >> 2] >> (8 * (e & 3))) & 3u;
-              G |= (unsigned long long)(bb & 1u) << (16 * q + e);
-              P |= (unsigned long long)(bb >> 1) << (16 * q + e);
+              for (int e = 0; e < 16; e++) {
+                const unsigned bb = (ws[e >> 2] >> (8 * (e & 3))) & 3u;
+                G |= (unsigned long long)(bb & 1u) << (16 * q + e);
+                P |= (unsigned long long)(bb >> 1) << (16 * q + e);
+              }
+            }
+          } else {  // NCHT = 8, 32: lane 0 only; the bits above NCHT propagate
+            P = ~0ull << NCHT;
+#pragma unroll
+            for (int e = 0; e < NCHT; e++) {
+              const unsigned bb = __ldcg(bits + e);
+              G |= (unsigned long long)(bb & 1u) << e;
+              P |= (unsigned long long)(bb >> 1) << e;
             }
           }
         }
@@ -401,12 +446,12 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
       __syncthreads();
 #pragma unroll 1
       for (int rd = 0; rd < ROUNDS; rd++) {
-        const int lc = rd * 16 + warp, ch = lc * C + (int)crank;
+        const int lc = rd * 16 + warp / TWP, ch = lc * C + (int)crank;
         const int kb = min(ch * WB, words), ke = min(kb + WB, words);
         const ChunkSrc src{coefL + lc * B, s_prev[lc], ch * B};
         // a one-warp team: the carry into the warp is the chunk's carry-in whatever
-        // the (stale) per-warp bits in seg say
-        carry_seg_emit(src, nc, nout, kb, ke, seg, s_cin[lc], out, warp, 1);
+        // the (stale) per-warp bits in seg say; larger teams use the scan's bits
+        carry_seg_emit(src, nc, nout, kb, ke, seg, s_cin[lc], out, w0, TWP);
       }
     } else {
       for (int lc = 0; lc < NCH; lc++) {

@@ -1,6 +1,7 @@
 """A/B device timing of two builds of libivm.so on the same GPU (dev tool).
 
     python tools/ab.py ab/libivm_base.so ab/libivm_new.so [--n 4096] [--batch 4096] [--rounds 5]
+    python tools/ab.py lib.so lib.so@IVM_KERNEL=v5      # same build, environment overrides
 
 Alternates the two builds in fresh subprocesses (one library per process) and
 prints the median ms per batch of each (CUDA events, L2 flushed between reps).
@@ -41,10 +42,11 @@ def main():
     ap.add_argument("--rounds", type=int, default=5)
     ap.add_argument("--reps", type=int, default=20)
     args = ap.parse_args()
-    res = {l: [] for l in args.libs}
+    res = {l: [] for l in dict.fromkeys(args.libs)}
     for _ in range(args.rounds):
         for lib in args.libs:
-            env = dict(os.environ, IVM_LIB=os.path.abspath(lib))
+            path, *kv = lib.split("@")
+            env = dict(os.environ, IVM_LIB=os.path.abspath(path), **dict(x.split("=", 1) for x in kv))
             o = subprocess.run([sys.executable, "-c", CHILD % (ROOT, args.n, args.batch, args.reps)], env=env,
                                capture_output=True, text=True, check=True)
             res[lib].append(json.loads(o.stdout.strip().splitlines()[-1]))
