@@ -161,26 +161,51 @@ template <int M> struct CoefCluster {
 // 4096 columns; x >= 0 is a point, so [x th.lo, x th.hi] needs no sign cases
 template <typename T, int M>
 __device__ __forceinline__ void cross_fwd(const uint8_t *__restrict__ dig, int n, Buf<T> st, const CI<T> *theta,
-                                          unsigned crank, bool wait_cluster = false) {
+                                          unsigned crank, bool wait_cluster, bool global) {
   constexpr int C = G4<M>::C;
   const int t = threadIdx.x;
   CI<T> acc[8];
 #pragma unroll
   for (int j = 0; j < 8; j++) acc[j] = CI<T>{T(0), T(0), T(0), T(0)};
+  auto mac = [&](CI<T> &a, T x, const CI<T> &th) {
+    a.rl = DR<T>::fma_rd(x, th.rl, a.rl);
+    a.rh = DR<T>::fma_ru(x, th.rh, a.rh);
+    a.il = DR<T>::fma_rd(x, th.il, a.il);
+    a.ih = DR<T>::fma_ru(x, th.ih, a.ih);
+  };
+  const bool odd = (crank & 1u) != 0u;
+  if (global && ((reinterpret_cast<uintptr_t>(dig) | (uintptr_t)n) & 3) == 0) {
+    // digits from L2 / HBM: word loads (the pass is bound by their latency), thread
+    // t owning columns 4t + e + 2048 h (e < 4, h < 2); with n % 4 == 0 a word is
+    // wholly inside or outside the digits.  (Staged digits keep the byte loads:
+    // the word form's 4-apart state stores conflict in shared memory.)
+#pragma unroll
+    for (int q = 0; q < C; q++) {
+      const CI<T> th = theta[q];
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int base = 4 * t + 2048 * h + 4096 * q;
+        const unsigned w = base < n ? *reinterpret_cast<const unsigned *>(dig + base) : 0u;
+#pragma unroll
+        for (int e = 0; e < 4; e++) mac(acc[4 * h + e], T((w >> (8 * e)) & 255u), th);
+      }
+    }
+    if (wait_cluster) cluster_wait();  // the previous pair's remote reads of this state are done
+#pragma unroll
+    for (int h = 0; h < 2; h++)
+#pragma unroll
+      for (int e = 0; e < 4; e++) st.st(4 * t + e + 2048 * h, odd ? cconj(acc[4 * h + e]) : acc[4 * h + e]);
+    return;
+  }
 #pragma unroll
   for (int q = 0; q < C; q++) {
     const CI<T> th = theta[q];
 #pragma unroll
     for (int j = 0; j < 8; j++) {
       const int idx = t + 512 * j + 4096 * q;
-      const T x = idx < n ? T(dig[idx]) : T(0);
-      acc[j].rl = DR<T>::fma_rd(x, th.rl, acc[j].rl);
-      acc[j].rh = DR<T>::fma_ru(x, th.rh, acc[j].rh);
-      acc[j].il = DR<T>::fma_rd(x, th.il, acc[j].il);
-      acc[j].ih = DR<T>::fma_ru(x, th.ih, acc[j].ih);
+      mac(acc[j], idx < n ? T(dig[idx]) : T(0), th);
     }
   }
-  const bool odd = (crank & 1u) != 0u;
   if (wait_cluster) cluster_wait();  // the previous pair's remote reads of this state are done
 #pragma unroll
   for (int j = 0; j < 8; j++) st.st(t + 512 * j, odd ? cconj(acc[j]) : acc[j]);
@@ -265,7 +290,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
     for (int op = 0; op < 2; op++) {
       if (staged) mbar_wait(&dbar, (unsigned)op);
       cross_fwd<T, M>(staged ? sdig : (op == 0 ? kp.a : kp.b) + (size_t)pair * n, n, st, theta, crank,
-                      op == 0 && it > 0);
+                      op == 0 && it > 0, !staged);
       if (op == 1 && threadIdx.x == 0) {
         cs.ok = 1;
         cs.first_bad = 0x7fffffff;

@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
     }
 #pragma unroll 1
     for (int op = 0; op < 2; op++) {
-      cross_fwd<T, M>((op == 0 ? kp.a : kp.b) + (size_t)pair * n, n, st, theta, crank);
+      cross_fwd<T, M>((op == 0 ? kp.a : kp.b) + (size_t)pair * n, n, st, theta, crank, false, true);
       if (op == 1 && threadIdx.x == 0) {
         cs.ok = 1;
         cs.first_bad = 0x7fffffff;
