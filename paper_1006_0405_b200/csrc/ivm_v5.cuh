@@ -438,9 +438,12 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
         const unsigned Gw = __ballot_sync(0xffffffffu, sg), Pw = __ballot_sync(0xffffffffu, sp);
         const unsigned cinl = ((((Gw | Pw) + Gw) ^ Pw) >> l) & 1u;
         const unsigned long long cb = ((G | P) + G + cinl) ^ P;  // carry into each chunk of the segment
-        for (int j = 0; j < 64; j++) {
-          const int ch = 64 * l + j;
-          if (ch < NCHT && ch % C == (int)crank) s_cin[ch / C] = (uint8_t)((cb >> j) & 1ull);
+        // own chunk lc (global ch = lc C + crank): bit ch % 64 of lane ch / 64's cb
+#pragma unroll
+        for (int h = 0; h < NCH; h += 32) {
+          const int lc = h + l, ch = lc * C + (int)crank;
+          const unsigned long long o = __shfl_sync(0xffffffffu, cb, min(ch >> 6, 31));
+          if (lc < NCH) s_cin[lc] = (uint8_t)((o >> (ch & 63)) & 1ull);
         }
       }
       __syncthreads();
