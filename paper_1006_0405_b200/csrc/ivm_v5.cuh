@@ -75,15 +75,18 @@ struct ChunkSrc {
   __device__ __forceinline__ unsigned long long one(int i) const { return get(i); }
 };
 
+// group barrier: the CTA's writes (ordered before thread 0 by the block barrier)
+// are released by thread 0's gpu-scope release add; the poll acquires the other
+// CTAs' releases
 __device__ __forceinline__ void gsync(unsigned *ctr, unsigned C, unsigned &gen) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
     const unsigned target = (gen + 1u) * C;
-    atomicAdd(ctr, 1u);
-    while (*(volatile unsigned *)ctr < target) {
-    }
-    __threadfence();
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    } while (v < target);
   }
   gen++;
   __syncthreads();
