@@ -79,10 +79,9 @@ template <typename F, int M> static int v4_tables_impl(const F *w2N /* [2m][4] *
       memcpy(out + 2L * (X::TH(c) + 2 * q), w2N + 4L * e, 4 * sizeof(F));  // full interval
     }
   }
-  for (int j = 0; j < C; j++) {  // w_C^{-j} and z^{-4096 j}
-    const long e1 = ((-(long)j * (N2 / C)) % N2 + N2) % N2, e2 = ((-(long)j * 4096) % N2 + N2) % N2;
-    memcpy(out + 2L * (X::S2 + 2 * j), w2N + 4L * e1, 4 * sizeof(F));
-    memcpy(out + 2L * (X::FO + 2 * j), w2N + 4L * e2, 4 * sizeof(F));
+  for (int j = 0; j < C; j++) {  // compact upper-half roots: w_C^j (2j <= C) or w_C^{C-j}; z^{4096 j}
+    put(X::S2 + 2 * j, (long)(2 * j <= C ? j : C - j) * (N2 / C));
+    put(X::FO + 2 * j, (long)j * 4096);
   }
   return ok ? X::TOTAL : -4;
 }

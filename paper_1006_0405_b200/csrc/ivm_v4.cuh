@@ -37,8 +37,10 @@ template <int M> struct G4 {
   //   INV:    local inverse passes 1..3: [7][8], [7][64], [7][512] (shared)
   //   XINV(c): role c, last inverse pass, [C][B] (rows c B .. c B + B - 1), folded untwist
   //   TH(c):  role c, theta_q (q < C) as full intervals (2 entries each)
-  //   S2:     w_C^{-j}, j < C (full intervals; v5's two-stage last inverse pass)
-  //   FO:     conj(w_{4C}^r) = z^{-4096 r}, r < C (full intervals; v5's emit)
+  //   S2:     j < C, compact at S2 + 2 j: w_C^j (2 j <= C) or w_C^{C-j}, the
+  //           upper-half-plane form of w_C^{-j} (v5's two-stage last inverse pass)
+  //   FO:     w_{4C}^r = z^{4096 r}, r < C (compact, first quadrant, at FO + 2 r;
+  //           v5's emit multiplies by its conjugate)
   __host__ __device__ static constexpr int FWD(int c) { return c * 4096; }
   __host__ __device__ static constexpr int FP(int p) { return p == 1 ? 0 : (p == 2 ? 7 : (p == 3 ? 63 : 512)); }
   static constexpr int INV = C * 4096;

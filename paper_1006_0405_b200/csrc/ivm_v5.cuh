@@ -105,12 +105,13 @@ template <typename T, int M> struct Cfg5 {
   static_assert(STATE_BYTES >= 8 * 8192, "int64 coefficients fit the state");
 };
 
-// c = 2 Re / m, 2 Im / m of t = w o (w: full interval), certified into d0, d1
+// c = 2 Re / m, 2 Im / m of t = conj(w) o (w: compact first-quadrant twiddle),
+// certified into d0, d1
 template <typename T, int M>
-__device__ __forceinline__ void emit_tab(const CI<T> &o, const CI<T> &w, int k, int n, long long *d0, long long *d1,
-                                         CertAcc &acc, double *dump) {
+__device__ __forceinline__ void emit_tab(const CI<T> &o, const TwC<T> &w, int k, int n, long long *d0,
+                                         long long *d1, CertAcc &acc, double *dump) {
   constexpr int N = 1 << M;
-  const CI<T> v = cmul(w, o);
+  const CI<T> v = rtmul<T, true, false>(w, o);
   const T s = T(2) / T(N);
   certify_real(DR<T>::mul_rd(v.rl, s), DR<T>::mul_ru(v.rh, s), k, n, d0, acc, dump);
   certify_real(DR<T>::mul_rd(v.il, s), DR<T>::mul_ru(v.ih, s), k + N / 2, n, d1, acc, dump);
@@ -132,8 +133,8 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
   Buf<T> st{reinterpret_cast<V *>(smem), reinterpret_cast<V *>(smem) + GL::CAP};
   TwC<T> *twb = reinterpret_cast<TwC<T> *>(smem + CF::STATE_BYTES);
   const CI<T> *theta = reinterpret_cast<const CI<T> *>(twb + X::S_TH);
-  const CI<T> *s2tw = reinterpret_cast<const CI<T> *>(twb + X::S_S2);
-  const CI<T> *fold = reinterpret_cast<const CI<T> *>(twb + X::S_FO);
+  const TwC<T> *s2tw = twb + X::S_S2;  // w_C^{-j}: s2tw[2 j], upper-half form (G4::S2)
+  const TwC<T> *fold = twb + X::S_FO;  // fold[2 r] = z^{4096 r}
   const unsigned crank = blockIdx.x % C;
   const int gi = (int)(blockIdx.x / C), ngr = (int)(gridDim.x / C);
   unsigned *ctr = g.ctr + gi;
@@ -267,7 +268,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
         const int kl = (int)threadIdx.x + 512 * g, k0 = (int)crank * B + kl;
 #pragma unroll
         for (int r = 0; r < C; r++)
-          emit_tab<T, M>(v[g][r], fold[r], k0 + 4096 * r, n, coefL + r * B + kl, coefL + (C + r) * B + kl, acc, dump);
+          emit_tab<T, M>(v[g][r], fold[2 * r], k0 + 4096 * r, n, coefL + r * B + kl, coefL + (C + r) * B + kl, acc, dump);
       }
     } else {
       // gather + input twiddles: y_q(kl) -> state[q B + kl]
@@ -288,7 +289,11 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
         for (int a = 0; a < 8; a++) v[a] = st.ld((C2 * a + b) * B + kl);
         cdft<T, 8, true>(v);
 #pragma unroll
-        for (int r1 = 1; r1 < 8; r1++) v[r1] = cmul(s2tw[b * r1], v[r1]);
+        for (int r1 = 1; r1 < 8; r1++) {  // b is warp-uniform (B >= 32)
+          const int j = b * r1;
+          const TwC<T> w = s2tw[2 * j];
+          v[r1] = 2 * j <= C ? rtmul<T, true, true>(w, v[r1]) : rtmul<T, false, true>(w, v[r1]);
+        }
         __syncthreads();
 #pragma unroll
         for (int r1 = 0; r1 < 8; r1++) st.st((r1 * C2 + b) * B + kl, v[r1]);
@@ -312,7 +317,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
 #pragma unroll
             for (int r2 = 0; r2 < C2; r2++) {
               const int r = r1 + 8 * r2, k = k0 + 4096 * r;
-              emit_tab<T, M>(v[r2], fold[r], k, n, coefL + r * B + kl, coefL + (C + r) * B + kl, acc, dump);
+              emit_tab<T, M>(v[r2], fold[2 * r], k, n, coefL + r * B + kl, coefL + (C + r) * B + kl, acc, dump);
             }
           }
         } else {
@@ -332,7 +337,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
 #pragma unroll
             for (int r2 = 0; r2 < C2; r2++) {
               const int r = r1 + 8 * r2, k = k0 + 4096 * r;
-              emit_tab<T, M>(v[g2][r2], fold[r], k, n, coefL + r * B + kl, coefL + (C + r) * B + kl, acc, dump);
+              emit_tab<T, M>(v[g2][r2], fold[2 * r], k, n, coefL + r * B + kl, coefL + (C + r) * B + kl, acc, dump);
             }
           }
         }
