@@ -224,7 +224,7 @@ template <typename T, int M> struct Cfg4 {
   static constexpr size_t DIG_BYTES = STATE_BYTES + TW_BYTES + (size_t)(1 << M) / 2 <= 227 * 1024 ? (1 << M) / 2 : 0;
   static constexpr size_t SMEM = STATE_BYTES + TW_BYTES + DIG_BYTES;
   static constexpr size_t A_BYTES = 2 * E * 4096;
-  static_assert(STATE_BYTES >= 4 * 8192, "local coefficients alias the state");
+  static_assert(sizeof(TwC<T>) * 4096 >= 4 * 8192, "local coefficients fit the twiddle swap buffer");
   static_assert(SMEM <= 227 * 1024, "shared memory");
 };
 
@@ -242,8 +242,10 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
   __shared__ unsigned s_cin[4];                         // carry into each of the 2C^2 chunks
   __shared__ __align__(8) unsigned long long tbar, dbar;
   Buf<T> st{reinterpret_cast<V *>(smem), reinterpret_cast<V *>(smem) + GL::CAP};
-  int32_t *coefL = reinterpret_cast<int32_t *>(smem);  // [2][C][B], aliases the state
   TwC<T> *twb = reinterpret_cast<TwC<T> *>(smem + CF::STATE_BYTES);
+  // [2][C][B] coefficients in the twiddle swap buffer (free after the last
+  // pass's twiddles are read): the state stays readable by the other CTAs
+  int32_t *coefL = reinterpret_cast<int32_t *>(twb + X::S_SWAP);
   const CI<T> *theta = reinterpret_cast<const CI<T> *>(twb + X::S_TH);
   uint8_t *sdig = smem + CF::STATE_BYTES + CF::TW_BYTES;
   const unsigned crank = cluster_rank();
@@ -293,6 +295,12 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
       if (staged) mbar_wait(&dbar, (unsigned)op);
       cross_fwd<T, M>(staged ? sdig : (op == 0 ? kp.a : kp.b) + (size_t)pair * n, n, st, theta, crank,
                       op == 0 && it > 0, !staged);
+      if (op == 0 && it > 0 && threadIdx.x == 0) {
+        // this pair's forward-last table into the swap buffer: the cluster wait in
+        // cross_fwd ordered every remote read of the previous coefficients before it
+        mbar_expect(&tbar, EB * X::FLAST);
+        bulk_copy(twb + X::S_SWAP, tw + X::FWD(crank) + X::FP(4), EB * X::FLAST, &tbar);
+      }
       if (op == 1 && threadIdx.x == 0) {
         cs.ok = 1;
         cs.first_bad = 0x7fffffff;
@@ -377,18 +385,23 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
           v[g][q] = (2 * q < C) ? z : cconj(z);
         }
       }
-      cluster_sync();  // (2) remote reads done: the state may be overwritten
+      // (no cluster barrier here: the coefficients do not overwrite the state)
       mbar_wait(&tbar, par);
-      double *dump = diag_dump(kp, pair, N);
 #pragma unroll
       for (int g = 0; g < G; g++) {
-        const int kl = (int)threadIdx.x + 512 * g, k0 = (int)crank * B + kl;
+        const int kl = (int)threadIdx.x + 512 * g;
 #pragma unroll
         for (int q = 0; q < C; q++) {
           const TwC<T> w = twb[X::S_SWAP + q * B + kl];
           v[g][q] = (2 * q < C) ? rtmul<T, true, true>(w, v[g][q]) : rtmul<T, false, true>(w, v[g][q]);
         }
         cdft<T, C, true>(v[g]);
+      }
+      __syncthreads();  // every twiddle read: the swap buffer takes the coefficients
+      double *dump = diag_dump(kp, pair, N);
+#pragma unroll
+      for (int g = 0; g < G; g++) {
+        const int kl = (int)threadIdx.x + 512 * g, k0 = (int)crank * B + kl;
 #pragma unroll
         for (int r = 0; r < C; r++)
           emit_fold<T, M, 4 * C>(v[g][r], r, k0 + 4096 * r, n, coefL + r * B + kl, coefL + (C + r) * B + kl, acc,
@@ -397,10 +410,6 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
     }
     cert_flush(acc, cs);
     __syncthreads();
-    if (threadIdx.x == 0 && pair + ncl < kp.batch) {  // next pair's forward-last table
-      mbar_expect(&tbar, EB * X::FLAST);
-      bulk_copy(twb + X::S_SWAP, tw + X::FWD(crank) + X::FP(4), EB * X::FLAST, &tbar);
-    }
     cluster_sync();  // (3) coefficients and per-CTA certificates complete
     // the C per-CTA certificates: lane p of warp 0 reads CTA p's, the warp
     // reduces, shared memory broadcasts (one remote read per CTA, not per thread)
@@ -487,8 +496,9 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
       if (kp.max_radius) kp.max_radius[pair] = __longlong_as_double((long long)rad);
       if (kp.first_bad) kp.first_bad[pair] = ok ? -1 : bad;
     }
-    // (5) remote coefficient / chunk-bit reads done before the next pair
-    // overwrites them: arrive now, wait just before the next state write
+    // (5) remote state / coefficient / chunk-bit reads done before the next pair
+    // overwrites them: arrive now, wait just before the next state write (and
+    // the next forward-last table, which replaces the coefficients)
     cluster_arrive_relaxed();
   }
   if (it > 0) cluster_wait();  // no CTA leaves while its shared memory may still be read
