@@ -161,7 +161,7 @@ template <int M> struct CoefCluster {
 
 // first (cross-CTA) forward pass from the digits: row `crank` of level 2C,
 // 4096 columns; x >= 0 is a point, so [x th.lo, x th.hi] needs no sign cases
-template <typename T, int M>
+template <typename T, int M, bool QB = false>
 __device__ __forceinline__ void cross_fwd(const uint8_t *__restrict__ dig, int n, Buf<T> st, const CI<T> *theta,
                                           unsigned crank, bool wait_cluster, bool global) {
   constexpr int C = G4<M>::C;
@@ -181,8 +181,7 @@ __device__ __forceinline__ void cross_fwd(const uint8_t *__restrict__ dig, int n
     // t owning columns 4t + e + 2048 h (e < 4, h < 2); with n % 4 == 0 a word is
     // wholly inside or outside the digits.  (Staged digits keep the byte loads:
     // the word form's 4-apart state stores conflict in shared memory.)
-#pragma unroll
-    for (int q = 0; q < C; q++) {
+    auto term = [&](int q) {
       const CI<T> th = theta[q];
 #pragma unroll
       for (int h = 0; h < 2; h++) {
@@ -191,6 +190,21 @@ __device__ __forceinline__ void cross_fwd(const uint8_t *__restrict__ dig, int n
 #pragma unroll
         for (int e = 0; e < 4; e++) mac(acc[4 * h + e], T((w >> (8 * e)) & 255u), th);
       }
+    };
+    // QB (a separate instantiation, chosen by the host when it skips a group):
+    // terms past ceil(n / 4096) multiply only zero padding and are skipped, in
+    // unrolled groups of 8.  Otherwise every term, fully unrolled (all loads in
+    // flight); one kernel holding both forms measured slower on both paths.
+    if constexpr (QB) {
+      const int qmax = (min(C, (n + 4095) >> 12) + 7) & ~7;
+#pragma unroll 1
+      for (int q0 = 0; q0 < qmax; q0 += 8) {
+#pragma unroll
+        for (int qq = 0; qq < 8; qq++) term(q0 + qq);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < C; q++) term(q);
     }
     if (wait_cluster) cluster_wait();  // the previous pair's remote reads of this state are done
 #pragma unroll

@@ -33,6 +33,11 @@ int upload_w64_v5(const double *w64, const float *w32) {  // this TU's DFT-inter
 template <typename T, int M> static int v5_info_impl(LaunchInfo *li) {
   using CF = v5::Cfg5<T, M>;
   auto k = v5::ivm_v5_kernel<T, M>;
+  if constexpr (M == 18) {  // the zero-padding-skipping variant (v5_go)
+    if (cudaFuncSetAttribute(v5::ivm_v5_kernel<T, M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)CF::SMEM) != cudaSuccess)
+      return -1;
+  }
   li->threads = CF::THREADS;
   li->smem = CF::SMEM;
   li->a_smem = false;
@@ -64,7 +69,11 @@ template <typename T, int M> static int v5_go(const KParams &kp, const Group5Arg
   KParams k2 = kp;
   v5::Group5 g{ga.ctr, ga.xch, ga.link, ga.bnd, ga.bits};
   void *args[] = {(void *)&k2, (void *)&g};
-  return cudaLaunchCooperativeKernel((const void *)v5::ivm_v5_kernel<T, M>, dim3(groups * v4::G4<M>::C),
+  // m = 2^18 with n <= 2^17 - 8 * 4096 (C3): the cross pass skips whole groups
+  // of zero-padding terms (a separate instantiation: ivm_v4.cuh cross_fwd)
+  const bool qb = M == 18 && kp.n <= (1 << (M - 1)) - 8 * 4096;
+  const void *fn = qb ? (const void *)v5::ivm_v5_kernel<T, M, M == 18> : (const void *)v5::ivm_v5_kernel<T, M>;
+  return cudaLaunchCooperativeKernel(fn, dim3(groups * v4::G4<M>::C),
                                      dim3(CF::THREADS), args, CF::SMEM, s) == cudaSuccess
              ? 0
              : -1;

@@ -117,7 +117,9 @@ __device__ __forceinline__ void emit_tab(const CI<T> &o, const TwC<T> &w, int k,
   certify_real(DR<T>::mul_rd(v.il, s), DR<T>::mul_ru(v.ih, s), k + N / 2, n, d1, acc, dump);
 }
 
-template <typename T, int M>
+// QB: the cross pass skips its zero-padding terms in groups of 8 (host picks it
+// when n <= m/2 - 8 * 4096, i.e. C3; ivm_v4.cuh cross_fwd)
+template <typename T, int M, bool QB = false>
 __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
   using X = G4<M>;
   using GL = G3<13, 8>;
@@ -173,7 +175,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
     }
 #pragma unroll 1
     for (int op = 0; op < 2; op++) {
-      cross_fwd<T, M>((op == 0 ? kp.a : kp.b) + (size_t)pair * n, n, st, theta, crank, false, true);
+      cross_fwd<T, M, QB>((op == 0 ? kp.a : kp.b) + (size_t)pair * n, n, st, theta, crank, false, true);
       if (op == 1 && threadIdx.x == 0) {
         cs.ok = 1;
         cs.first_bad = 0x7fffffff;
