@@ -8,6 +8,8 @@ code with the CUDA path (paper_1006_0405_b200/); the product never imports it.
   coefficient sums P:37, carry P:229-235, and the paper's interval
   Schoenhage-Strassen multiply (P:143-155 FFT, P:203-211 fast convolution,
   P:250-265 interval arithmetic) with fesetround directed rounding.
+- ``ivm_oracle_disc.c`` (same library): the circular-containment-set variant the
+  paper proposes as future work, disc arithmetic per DESIGN.md reading R15.
 - ``twiddles.py``: optimal enclosures of omega_N^j from mpmath.
 
 Parity status: every function here is pinned by ``tests/test_oracle_*.py``
@@ -29,6 +31,7 @@ from .twiddles import twiddle_table, direct_enclosure  # noqa: F401
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
 _SRC = os.path.join(_HERE, "ivm_oracle.c")
+_SRCS = [_SRC, os.path.join(_HERE, "ivm_oracle_disc.c")]
 
 CFLAGS = ["-O2", "-fPIC", "-shared", "-fopenmp", "-frounding-math", "-ffp-contract=off",
           "-fno-fast-math", "-std=c11", "-Wall", "-Wno-unknown-pragmas",
@@ -37,8 +40,8 @@ CFLAGS = ["-O2", "-fPIC", "-shared", "-fopenmp", "-frounding-math", "-ffp-contra
 
 def build(force: bool = False) -> str:
     """Compile liboracle.so (gcc) if missing or stale."""
-    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", *CFLAGS, _SRC, "-o", _SO, "-lm"])
+    if force or not os.path.exists(_SO) or any(os.path.getmtime(_SO) < os.path.getmtime(f) for f in _SRCS):
+        subprocess.check_call(["gcc", *CFLAGS, *_SRCS, "-o", _SO, "-lm"])
     return _SO
 
 
@@ -67,6 +70,10 @@ def lib():
         L.oracle_fft_length.restype = S
         L.oracle_certify_f64.argtypes = [P, S, P, P]
         L.oracle_self_check.restype = I
+        L.oracle_disc_batch.argtypes = [P, P, S, S, P, P, P, P, P, P, P, I]
+        L.oracle_disc_batch.restype = I
+        L.oracle_disc_op.argtypes = [I, P, P, P, S]
+        L.oracle_disc_fft.argtypes = [P, P, P, S, I]
         L.oracle_max_threads.restype = I
         _lib = L
     return _lib
@@ -109,6 +116,51 @@ def ivmul(a: np.ndarray, b: np.ndarray, prec: str = "f64", want_coeffs: bool = F
     assert rc == 0
     return {"prod": prod, "cert": cert.astype(bool), "max_radius": rad, "first_bad": bad,
             "coeffs": coeffs, "intervals": ivs, "N": N}
+
+
+def disc_mul(a: np.ndarray, b: np.ndarray, want_coeffs: bool = False, want_discs: bool = False,
+             nthreads: int = 0) -> dict:
+    """The multiply with circular containment sets (R15), fp64,
+    on a batch [B][n] of digit pairs.  max_radius = the largest disc radius over
+    the used coefficients; discs [B][N][3] = (center re, center im, radius)."""
+    a = np.ascontiguousarray(a, dtype=np.uint8)
+    b = np.ascontiguousarray(b, dtype=np.uint8)
+    if a.ndim == 1:
+        a, b = a[None], b[None]
+    B, n = a.shape
+    N = fft_length(n)
+    tw = np.ascontiguousarray(twiddle_table(N, "f64"))
+    prod = np.zeros((B, 2 * n), np.uint8)
+    cert = np.zeros(B, np.uint8)
+    rad = np.zeros(B, np.float64)
+    bad = np.zeros(B, np.int32)
+    coeffs = np.zeros((B, 2 * n - 1), np.int64) if want_coeffs else None
+    discs = np.zeros((B, N, 3), np.float64) if want_discs else None
+    rc = lib().oracle_disc_batch(_p(a), _p(b), n, B, _p(tw), _p(prod), _p(cert), _p(rad), _p(bad),
+                                 _p(coeffs), _p(discs), nthreads)
+    assert rc == 0
+    return {"prod": prod, "cert": cert.astype(bool), "max_radius": rad, "first_bad": bad,
+            "coeffs": coeffs, "discs": discs, "N": N}
+
+
+def disc_op(op: str, a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """Disc primitive (R15) on [len][3] arrays: add, sub, mul, conj."""
+    code = {"add": 0, "sub": 1, "mul": 2, "conj": 3}[op]
+    a = np.ascontiguousarray(a, np.float64)
+    b = np.ascontiguousarray(b, np.float64)
+    r = np.zeros_like(a)
+    lib().oracle_disc_op(code, _p(a), _p(b), _p(r), a.shape[0])
+    return r
+
+
+def disc_fft(x: np.ndarray, inverse: int = 0) -> np.ndarray:
+    """The paper's recursive FFT on discs [N][3], unscaled."""
+    x = np.ascontiguousarray(x, np.float64)
+    N = x.shape[0]
+    tw = np.ascontiguousarray(twiddle_table(N, "f64"))
+    out = np.zeros_like(x)
+    lib().oracle_disc_fft(_p(x), _p(out), _p(tw), N, inverse)
+    return out
 
 
 def long_multiply(a: np.ndarray, b: np.ndarray, nthreads: int = 0) -> np.ndarray:
