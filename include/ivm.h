@@ -162,6 +162,19 @@ int ivm_multiply_exact(ivm_ctx_t ctx, const uint8_t *a, const uint8_t *b, size_t
 int ivm_multiply_naive(ivm_ctx_t ctx, const uint8_t *a, const uint8_t *b, size_t n, size_t batch,
                        uint8_t *prod, int prec, void *cuda_stream);
 
+/* Circular containment sets (the paper's suggested future work;
+ * SURVEY §8(f) rank 4): the same multiplication (radix-2 DIT FFT P:143-155,
+ * pointwise product P:210, inverse P:97/P:211, unique-integer rule P:24, carry
+ * P:229-235) with every complex value a disc <c, r> = {z : |z - c| <= r}:
+ * round-to-nearest centers, round-up radius bounds (reading R15).
+ * fp64.  a, b: device [batch][n]; prod: device [batch][2n] (zero digits where
+ * not certified); cert: device [batch] (1 = proved exact); max_radius:
+ * device [batch] largest disc radius over the 2n-1 used coefficients, or NULL.
+ * n <= 4096 (m <= 8192; IVM_EUNSUPPORTED otherwise).  Asynchronous on
+ * `cuda_stream`; uses context-owned device scratch. */
+int ivm_multiply_disc(ivm_ctx_t ctx, const uint8_t *a, const uint8_t *b, size_t n, size_t batch,
+                      uint8_t *prod, uint8_t *cert, double *max_radius, void *cuda_stream);
+
 /* Single-process multi-GPU: one context per device plus NCCL
  * communicators (ncclCommInitAll; NCCL is dlopen'ed, "libnccl.so.2").
  * devices: [ngpu] CUDA ordinals, devices[0] is the root.  IVM_ENCCL if NCCL

@@ -23,8 +23,8 @@ EXPORTS = ["ivm_version", "ivm_strerror", "ivm_max_digits", "ivm_fft_length", "i
            "ivm_destroy", "ivm_reserve", "ivm_multiply", "ivm_multiply_batched",
            "ivm_multiply_batched_diag", "ivm_multiply_batched_host", "ivm_generate_digits",
            "ivm_peak_probe", "ivm_last_launch_count", "ivm_twiddle_table", "ivm_long_multiply_batched",
-           "ivm_multiply_exact", "ivm_multiply_naive", "ivm_multi_create", "ivm_multi_multiply",
-           "ivm_multi_destroy"]
+           "ivm_multiply_exact", "ivm_multiply_naive", "ivm_multiply_disc", "ivm_multi_create",
+           "ivm_multi_multiply", "ivm_multi_destroy"]
 
 
 class IvmError(RuntimeError):
@@ -60,6 +60,7 @@ def lib():
             "ivm_long_multiply_batched": ([P, P, P, S, S, P, P], None),
             "ivm_multiply_exact": ([P, P, P, S, S, P, P, I, P], None),
             "ivm_multiply_naive": ([P, P, P, S, S, P, I, P], None),
+            "ivm_multiply_disc": ([P, P, P, S, S, P, P, P, P], None),
             "ivm_multi_create": ([ctypes.POINTER(P), I, P], None),
             "ivm_multi_multiply": ([P, P, P, S, S, P, P, I, I, P, P], None),
             "ivm_multi_destroy": ([P], None),
@@ -190,6 +191,20 @@ class Context:
         _check(lib().ivm_multiply_naive(self._h, _ptr(a), _ptr(b), n, B, _ptr(out), prec, _stream(stream)),
                "ivm_multiply_naive")
         return out
+
+    def multiply_disc(self, a, b, out=None, cert=None, want_radius: bool = True, stream=None):
+        """Circular containment sets (R15), fp64, n <= 4096:
+        (products [B][2n] u8, certified [B] u8, max disc radius [B] f64 or None)."""
+        import torch
+        B, n = a.shape
+        if out is None:
+            out = torch.empty((B, 2 * n), dtype=torch.uint8, device=a.device)
+        if cert is None:
+            cert = torch.empty((B,), dtype=torch.uint8, device=a.device)
+        rad = torch.empty((B,), dtype=torch.float64, device=a.device) if want_radius else None
+        _check(lib().ivm_multiply_disc(self._h, _ptr(a), _ptr(b), n, B, _ptr(out), _ptr(cert), _ptr(rad),
+                                       _stream(stream)), "ivm_multiply_disc")
+        return out, cert, rad
 
     def long_multiply(self, a, b, out=None, stream=None):
         """Exact long multiplication on the device: [B][2n] u8."""

@@ -23,7 +23,7 @@ NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--ft
 CXXFLAGS = ["-O2", "-fPIC", "-std=gnu++17", "-fext-numeric-literals", "-I", os.path.join(ROOT, "include"),
             "-I", os.path.join(os.path.dirname(os.path.dirname(NVCC)), "include")]
 
-CU = ["ivm_kernels.cu", "ivm_v3.cu", "ivm_v4.cu", "ivm_v5.cu", "ivm_long.cu", "ivm_naive.cu", "ivm_api.cu"]
+CU = ["ivm_kernels.cu", "ivm_v3.cu", "ivm_v4.cu", "ivm_v5.cu", "ivm_long.cu", "ivm_naive.cu", "ivm_disc.cu", "ivm_api.cu"]
 CPP = ["ivm_planner.cpp", "ivm_multi.cpp"]
 # every header under csrc/ is a dependency of every translation unit
 HDR = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))

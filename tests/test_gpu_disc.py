@@ -1,0 +1,71 @@
+"""GPU circular-containment-set multiply (ivm_multiply_disc, DESIGN.md
+R15) against the disc oracle (oracle/ivm_oracle_disc.c) on the same seeded
+inputs: products bit-exact with the schoolbook oracle, the certified flag equal
+wherever the oracle certifies with margin, the GPU disc radius within 2x of the
+oracle's (both directions reported), uncertified products zero."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1006_0405_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import paper_1006_0405_b200 as ivm
+    return ivm.Context(0)
+
+
+def run(ctx, a, b):
+    import torch
+    p, c, r = ctx.multiply_disc(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
+    return p.cpu().numpy(), c.cpu().numpy().astype(bool), r.cpu().numpy()
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 31, 100, 513, 1000, 2048, 4096])
+def test_disc_parity_with_oracle(ctx, n):
+    K = inputs.KINDS
+    B = 12
+    kinds = np.array([K["uniform"], K["all255"], K["sparse"], K["msd"]])[np.arange(B) % 4]
+    a, b = inputs.pair_digits(0xD15C + n, np.arange(B), n, kinds)
+    prod, cert, rad = run(ctx, a, b)
+    ref = oracle.disc_mul(a, b)
+    exact = oracle.long_multiply(a, b)
+    margin = ref["max_radius"] < 0.25
+    assert np.array_equal(cert[margin], ref["cert"][margin])
+    assert np.array_equal(prod[cert], exact[cert])
+    assert not prod[~cert].any()
+    ratio = rad / np.maximum(ref["max_radius"], 1e-300)
+    assert (ratio <= 2.0).all(), (n, ratio.max())
+    assert (ratio >= 0.25).all(), (n, ratio.min())  # not suspiciously tight either
+
+
+def test_disc_all_255_closed_form(ctx):
+    n = 4096
+    a = np.full((2, n), 255, np.uint8)
+    prod, cert, _ = run(ctx, a, a)
+    want = np.concatenate([[1], np.zeros(n - 1), [254], np.full(n - 1, 255)]).astype(np.uint8)
+    assert cert.all() and (prod == want).all()
+
+
+def test_disc_batch_ragged_and_deterministic(ctx):
+    """A batch larger than the grid (several pairs per CTA), odd n; two runs
+    bitwise identical (products, flags and radii)."""
+    n = 777
+    a, b = inputs.pair_digits(0xD15D, np.arange(600), n, "uniform")
+    p1, c1, r1 = run(ctx, a, b)
+    p2, c2, r2 = run(ctx, a, b)
+    assert np.array_equal(p1, p2) and np.array_equal(c1, c2) and np.array_equal(r1, r2)
+    assert c1.all()
+    sel = np.arange(0, 600, 37)
+    assert np.array_equal(p1[sel], oracle.long_multiply(a[sel], b[sel]))
+
+
+def test_disc_rejects_too_large(ctx):
+    import torch
+    import paper_1006_0405_b200 as ivm
+    t = torch.zeros((1, 4097), dtype=torch.uint8, device="cuda")
+    with pytest.raises(ivm.IvmError):
+        ctx.multiply_disc(t, t)
