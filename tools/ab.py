@@ -2,6 +2,7 @@
 
     python tools/ab.py ab/libivm_base.so ab/libivm_new.so [--n 4096] [--batch 4096] [--rounds 5]
     python tools/ab.py lib.so lib.so@IVM_KERNEL=v5      # same build, environment overrides
+    AB_FN=disc python tools/ab.py ...                   # time ivm_multiply_disc instead
 
 Alternates the two builds in fresh subprocesses (one library per process) and
 prints the median ms per batch of each (CUDA events, L2 flushed between reps).
@@ -24,11 +25,16 @@ n, B, reps = %d, %d, %d
 a = ctx.generate_digits(n, B, 1, 0); b = ctx.generate_digits(n, B, 1, 1)
 out = torch.empty((B, 2 * n), dtype=torch.uint8, device="cuda"); cert = torch.empty((B,), dtype=torch.uint8, device="cuda")
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-for _ in range(3): ctx.multiply(a, b, out=out, cert=cert)
+import os
+if os.environ.get("AB_FN") == "disc":
+    mul = lambda: ctx.multiply_disc(a, b, out=out, cert=cert, want_radius=False)
+else:
+    mul = lambda: ctx.multiply(a, b, out=out, cert=cert)
+for _ in range(3): mul()
 ts = []
 for _ in range(reps):
     flush.zero_(); e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(); ctx.multiply(a, b, out=out, cert=cert); e1.record(); torch.cuda.synchronize()
+    e0.record(); mul(); e1.record(); torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))
 print(json.dumps(sorted(ts)[len(ts) // 2]))
 """
