@@ -69,6 +69,13 @@ struct ChunkSrc {
                       : (i >= first - 8 ? (unsigned long long)prev8[i - first + 8] : 0ull);
   }
   __device__ __forceinline__ void quad(int k, unsigned long long (&o)[4]) const {
+    if (4 * k >= first) {  // wholly local (first and local are 32-byte aligned): two 16-byte loads
+      const longlong2 *q = reinterpret_cast<const longlong2 *>(local + (4 * k - first));
+      const longlong2 x = q[0], y = q[1];
+      o[0] = (unsigned long long)x.x, o[1] = (unsigned long long)x.y;
+      o[2] = (unsigned long long)y.x, o[3] = (unsigned long long)y.y;
+      return;
+    }
 #pragma unroll
     for (int e = 0; e < 4; e++) o[e] = get(4 * k + e);
   }
@@ -365,10 +372,18 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
       link[crank * 8 + 3] = (unsigned)(cs.maxrad >> 32);
     }
     gsync(ctr, C, gen);  // (2) certificates and chunk boundaries of every CTA visible
-    // the group's certificate: one warp reads the C link records (L2) and broadcasts
+    // the group's certificate: warp 0 reads the C link records (L2) and broadcasts;
+    // meanwhile the other warps fetch the boundary coefficients before each own chunk
     __shared__ int s_ok, s_bad;
     __shared__ unsigned long long s_rad;
-    if (threadIdx.x < 32) {
+    __shared__ uint8_t s_cin[64];
+    __shared__ long long s_prev[64][8];
+    if (threadIdx.x >= 32) {
+      for (int e = (int)threadIdx.x - 32; e < NCH * 8; e += (int)blockDim.x - 32) {
+        const int lc = e / 8, ch = lc * C + (int)crank;
+        s_prev[lc][e % 8] = ch > 0 ? __ldcg(bnd + (size_t)(ch - 1) * 8 + e % 8) : 0ll;
+      }
+    } else {
       const unsigned l = threadIdx.x;
       int okl = 1, badl = 0x7fffffff;
       unsigned long long radl = 0ull;
@@ -396,13 +411,6 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
     const unsigned long long rad = s_rad;
     const int words = (nout + 3) / 4, warp = (int)threadIdx.x >> 5;
     uint8_t *out = kp.prod + (size_t)pair * nout;
-    __shared__ uint8_t s_cin[64];
-    __shared__ long long s_prev[64][8];  // boundary coefficients before each own chunk
-    for (int e = (int)threadIdx.x; e < NCH * 8; e += blockDim.x) {
-      const int lc = e / 8, ch = lc * C + (int)crank;
-      s_prev[lc][e % 8] = ch > 0 ? __ldcg(bnd + (size_t)(ch - 1) * 8 + e % 8) : 0ll;
-    }
-    __syncthreads();
     const int w0 = warp / TWP * TWP;  // first warp of this thread's team
 #pragma unroll 1
     for (int rd = 0; rd < ROUNDS; rd++) {
