@@ -128,11 +128,9 @@ static __device__ __forceinline__ void carry_seg_scan(const Src &src, int nc, in
     cs.wp[w0 + warp] = ap ? 1u : 0u;
   }
   __syncthreads();
-  unsigned G2 = 0, P2 = 0;
-  for (unsigned w = 0; w < nwarps; w++) {
-    G2 |= (cs.wg[w0 + w] != 0u ? 1u : 0u) << w;
-    P2 |= (cs.wp[w0 + w] != 0u ? 1u : 0u) << w;
-  }
+  // the team's per-warp bits: lane w reads warp w's, two ballots gather them
+  const bool gw = lane < nwarps && cs.wg[w0 + lane] != 0u, pw = lane < nwarps && cs.wp[w0 + lane] != 0u;
+  const unsigned G2 = __ballot_sync(0xffffffffu, gw), P2 = __ballot_sync(0xffffffffu, pw);
   const unsigned long long S = (unsigned long long)(G2 | P2) + G2;
   gen = (unsigned)(S >> nwarps) & 1u;
   allp = (nwarps == 32 ? P2 == 0xffffffffu : P2 == ((1u << nwarps) - 1u)) ? 1u : 0u;
@@ -146,11 +144,9 @@ static __device__ __forceinline__ void carry_seg_emit(const Src &src, int nc, in
   const unsigned nwarps = nw ? (unsigned)nw : blockDim.x >> 5, warp = (threadIdx.x >> 5) - (unsigned)w0;
   const int J = (ke - kb + 32 * (int)nwarps - 1) / (32 * (int)nwarps);
   const int k0 = kb + (int)warp * 32 * J;
-  unsigned G2 = 0, P2 = 0;
-  for (unsigned w = 0; w < nwarps; w++) {
-    G2 |= (cs.wg[w0 + w] != 0u ? 1u : 0u) << w;
-    P2 |= (cs.wp[w0 + w] != 0u ? 1u : 0u) << w;
-  }
+  const bool gw = nw != 1 && lane < nwarps && cs.wg[w0 + lane] != 0u;
+  const bool pw = nw != 1 && lane < nwarps && cs.wp[w0 + lane] != 0u;
+  const unsigned G2 = __ballot_sync(0xffffffffu, gw), P2 = __ballot_sync(0xffffffffu, pw);
   const unsigned long long S0 = (unsigned long long)(G2 | P2) + G2 + cin;
   unsigned c = nw == 1 ? cin : (unsigned)((S0 ^ P2) >> warp) & 1u;  // carry into this warp's sub-segment
   unsigned hp, ep;
