@@ -325,6 +325,15 @@ __device__ __forceinline__ unsigned ld_shared_u8(const uint8_t *p) {
   return v;
 }
 // SMEMDIG: the digits are in shared memory (staged), else global
+// a digit (< 256) as T without an I2F: (2^52 + x) - 2^52 (fp32: 2^23), exact
+template <typename T> __device__ __forceinline__ T digit_val(unsigned x);
+template <> __device__ __forceinline__ double digit_val<double>(unsigned x) {
+  return __dsub_rn(__hiloint2double(0x43300000, (int)x), 4503599627370496.0);
+}
+template <> __device__ __forceinline__ float digit_val<float>(unsigned x) {
+  return __fsub_rn(__int_as_float(0x4B000000 | (int)x), 8388608.0f);
+}
+
 template <typename T, int M, int RK, bool SMEMDIG = false>
 __device__ __forceinline__ void fwd_first(const uint8_t *__restrict__ dig, int n, Buf<T> st,
                                           const TwC<T> *__restrict__ tw, int tid = threadIdx.x) {
@@ -339,7 +348,8 @@ __device__ __forceinline__ void fwd_first(const uint8_t *__restrict__ dig, int n
 #pragma unroll
       for (int q = 0; q < R; q++) {
         const int idx = nu + Sp * q;
-        const T x = idx < n ? T(SMEMDIG ? ld_shared_u8(dig + idx) : (unsigned)dig[idx]) : T(0);
+        const unsigned dv = idx < n ? (SMEMDIG ? ld_shared_u8(dig + idx) : (unsigned)dig[idx]) : 0u;
+        const T x = digit_val<T>(dv);
         if (q == 0) {
           v[g][q] = punctual(x);
         } else {
