@@ -319,12 +319,8 @@ template <typename T> struct Buf {
 // ---------------------------------------------------------------------------
 // pass 1: G_1[0][v] = x[v] (the trivial radix-2 pass 0), read from HBM;
 // G_2[2r][v] = sum_q w_R^{qr} (w_{4R}^q x[v + S'q]), stored with the mirror.
-__device__ __forceinline__ unsigned ld_shared_u8(const uint8_t *p) {
-  unsigned v;
-  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)));
-  return v;
-}
-// SMEMDIG: the digits are in shared memory (staged), else global
+// SMEMDIG: the digits are in shared memory (staged; the compiler emits LDS for
+// them), else global
 // a digit (< 256) as T without an I2F: (2^52 + x) - 2^52 (fp32: 2^23), exact
 template <typename T> __device__ __forceinline__ T digit_val(unsigned x);
 template <> __device__ __forceinline__ double digit_val<double>(unsigned x) {
@@ -348,7 +344,7 @@ __device__ __forceinline__ void fwd_first(const uint8_t *__restrict__ dig, int n
 #pragma unroll
       for (int q = 0; q < R; q++) {
         const int idx = nu + Sp * q;
-        const unsigned dv = idx < n ? (SMEMDIG ? ld_shared_u8(dig + idx) : (unsigned)dig[idx]) : 0u;
+        const unsigned dv = idx < n ? (unsigned)dig[idx] : 0u;
         const T x = digit_val<T>(dv);
         if (q == 0) {
           v[g][q] = punctual(x);
