@@ -31,7 +31,7 @@ struct ivm_ctx {
   std::map<std::pair<int, int>, void *> tw4;  // (log2m, prec) -> v4 role tables
   std::map<std::pair<int, int>, ivm::LaunchInfo> info4;
   std::map<std::pair<int, int>, void *> twn;  // (log2m, prec) -> round-to-nearest twiddles (naive SS)
-  std::map<int, void *> twd;                 // log2m -> twiddle discs (circular sets)
+  std::map<int, std::pair<void *, double>> twd;  // log2m -> twiddle disc centers + radius bound
   void *dscratch = nullptr;                  // circular sets: per-CTA spectrum of a
   size_t dscratch_bytes = 0;
   void *nscratch = nullptr;                  // naive SS: per-CTA spectrum of a
@@ -146,7 +146,7 @@ int ivm_destroy(ivm_ctx_t c) {
   for (auto &kv : c->tw3) cudaFree(kv.second);
   for (auto &kv : c->tw4) cudaFree(kv.second);
   for (auto &kv : c->twn) cudaFree(kv.second);
-  for (auto &kv : c->twd) cudaFree(kv.second);
+  for (auto &kv : c->twd) cudaFree(kv.second.first);
   cudaFree(c->dscratch);
   cudaFree(c->nscratch);
   cudaFree(c->ascratch);
@@ -809,24 +809,26 @@ int ivm_multiply_disc(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, size_t n,
   if (cudaSetDevice(c->device) != cudaSuccess) return cuda_fail(c);
   const int lg = log2m_for(n);  // n = 1: m = 1 (no FFT stage)
   void *w = nullptr;
+  double rw = 0.0;
   auto it = c->twd.find(lg);
   if (it != c->twd.end()) {
-    w = it->second;
-  } else {  // twiddle discs from the optimal rectangles: c = lower corner, r >= its diagonal
+    w = it->second.first;
+    rw = it->second.second;
+  } else {  // twiddle discs from the optimal rectangles: c = lower corner, r >= its diagonal (max over j)
     const size_t m = (size_t)1 << lg;
-    std::vector<double> rect(m * 4), h(m < 2 ? 4 : m / 2 * 4, 0.0);
+    std::vector<double> rect(m * 4), h(m < 2 ? 2 : m, 0.0);
     if (ivm::plan_twiddles(lg, IVM_F64, rect.data()) != 0) return IVM_EUNSUPPORTED;
     for (size_t j = 0; j < m / 2; j++) {
       const double *t = &rect[4 * j];
-      h[4 * j] = t[0];
-      h[4 * j + 1] = t[2];
-      h[4 * j + 2] = std::nextafter((t[1] - t[0]) + (t[3] - t[2]), 1.0);  // exact differences, sum rounded up
-      h[4 * j + 3] = 0.0;
+      h[2 * j] = t[0];
+      h[2 * j + 1] = t[2];
+      const double r = std::nextafter((t[1] - t[0]) + (t[3] - t[2]), 1.0);  // exact differences, sum rounded up
+      rw = r > rw ? r : rw;
     }
     if (cudaMalloc(&w, h.size() * sizeof(double)) != cudaSuccess) return IVM_ENOMEM;
     if (cudaMemcpy(w, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
       return cuda_fail(c);
-    c->twd[lg] = w;
+    c->twd[lg] = std::make_pair(w, rw);
   }
   size_t grid = (size_t)c->sms;
   if (grid > batch) grid = batch;
@@ -838,7 +840,7 @@ int ivm_multiply_disc(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, size_t n,
     if (cudaMalloc(&c->dscratch, need) != cudaSuccess) return IVM_ENOMEM;
     c->dscratch_bytes = need;
   }
-  if (ivm::disc_launch(a, b, (int)n, (int)batch, lg, w, c->dscratch, prod, cert, max_radius, (int)grid,
+  if (ivm::disc_launch(a, b, (int)n, (int)batch, lg, w, rw, c->dscratch, prod, cert, max_radius, (int)grid,
                        (cudaStream_t)stream) != 0)
     return cuda_fail(c);
   c->last_launches = 1;

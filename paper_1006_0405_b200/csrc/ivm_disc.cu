@@ -6,7 +6,8 @@
 // A disc <c, r> = { z : |z - c| <= r }.  Arithmetic (reading R15):
 // centers are round-to-nearest binary64 operations; radii are upper bounds in
 // round-up arithmetic, U = 2^-52 bounds one rounding relative to its result,
-// ETA = 2^-1000 guards subnormals:
+// ETA = 2^-1000 guards subnormals (radii are kept as binary32 rounded up, and
+// every twiddle disc uses the largest twiddle radius):
 //   sum        <a.c +- b.c, a.r + b.r + U (|s.re| + |s.im|) + 2 ETA>
 //   product    t1..t4 = the four center products, p = (t1 - t2, t3 + t4),
 //              r = |a.c| b.r + |b.c| a.r + a.r b.r + U (sum of |t_i| and |p|) + 6 ETA
@@ -59,16 +60,19 @@ __device__ __forceinline__ Disc dmul(const Disc &a, const Disc &b, double na, do
 }
 __device__ __forceinline__ double l1(const Disc &a) { return ru_add(fabs(a.cr), fabs(a.ci)); }
 
-struct SDisc {  // shared-memory planes: centers (double2) and radii
+// disc planes: centers (double2) and radii stored as binary32 rounded up (an
+// upper bound again: sound), 20 bytes per disc, so that the m = 8192 state and
+// the twiddle centers fit in shared memory together
+struct SDisc {
   double2 *c;
-  double *r;
+  float *r;
   __device__ __forceinline__ Disc ld(int i) const {
     const double2 v = c[i];
-    return Disc{v.x, v.y, r[i]};
+    return Disc{v.x, v.y, (double)r[i]};
   }
   __device__ __forceinline__ void st(int i, const Disc &d) const {
     c[i] = make_double2(d.cr, d.ci);
-    r[i] = d.r;
+    r[i] = __double2float_ru(d.r);
   }
 };
 
@@ -76,17 +80,20 @@ __device__ __forceinline__ int brev(int j, int lg) { return lg ? (int)(__brev((u
 
 // P:143-155 iteratively: stage s combines half-length-2^s transforms; the
 // twiddle of butterfly j is omega_{2^{s+1}}^j = omega_m^{j m / 2^{s+1}}
+// tw: twiddle centers omega_m^j (j < m/2) in shared memory; rw: one radius
+// bound for all of them (the host's max over j)
 template <bool INV>
-__device__ __forceinline__ void dfft(SDisc x, int lg, const double4 *__restrict__ tw) {
+__device__ __forceinline__ void dfft(SDisc x, int lg, const double2 *tw, double rw) {
   const int m = 1 << lg;
+  const double nw = ru_add(1.0, rw);
   for (int s = 0; s < lg; s++) {
     const int half = 1 << s, stride = m >> (s + 1);
     for (int b = threadIdx.x; b < m / 2; b += blockDim.x) {
       const int j = b & (half - 1), i0 = ((b >> s) << (s + 1)) + j, i1 = i0 + half;
-      const double4 t = tw[j * stride];  // (c.re, c.im, r, -)
-      const Disc w{t.x, INV ? -t.y : t.y, t.z};
+      const double2 t = tw[j * stride];
+      const Disc w{t.x, INV ? -t.y : t.y, rw};
       const Disc o = x.ld(i1), e = x.ld(i0);
-      const Disc wo = dmul(w, o, ru_add(1.0, t.z), l1(o));
+      const Disc wo = dmul(w, o, nw, l1(o));
       x.st(i0, dsum(e, wo, false));
       x.st(i1, dsum(e, wo, true));
     }
@@ -96,13 +103,15 @@ __device__ __forceinline__ void dfft(SDisc x, int lg, const double4 *__restrict_
 
 __global__ void __launch_bounds__(TH, 1)
     disc_kernel(const uint8_t *__restrict__ a, const uint8_t *__restrict__ b, int n, int batch, int lg,
-                const double4 *__restrict__ tw, double *__restrict__ scratch, uint8_t *__restrict__ prod,
-                uint8_t *__restrict__ cert, double *__restrict__ max_radius) {
+                const double2 *__restrict__ twg, double rw, double *__restrict__ scratch,
+                uint8_t *__restrict__ prod, uint8_t *__restrict__ cert, double *__restrict__ max_radius) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int m = 1 << lg, nc = 2 * n - 1;
-  SDisc x{reinterpret_cast<double2 *>(smem), reinterpret_cast<double *>(smem + 16 * (size_t)m)};
+  SDisc x{reinterpret_cast<double2 *>(smem), reinterpret_cast<float *>(smem + 16 * (size_t)m)};
+  double2 *tw = reinterpret_cast<double2 *>(smem + ((20 * (size_t)m + 15) & ~(size_t)15));  // m/2 centers
+  for (int j = threadIdx.x; j < m / 2; j += blockDim.x) tw[j] = twg[j];
   SDisc A{reinterpret_cast<double2 *>(scratch) + (size_t)blockIdx.x * 2 * m, nullptr};
-  A.r = reinterpret_cast<double *>(A.c + m);
+  A.r = reinterpret_cast<float *>(A.c + m);
   __shared__ int s_ok;
   __shared__ unsigned long long s_rad;
   for (int pair = blockIdx.x; pair < batch; pair += gridDim.x) {
@@ -114,7 +123,7 @@ __global__ void __launch_bounds__(TH, 1)
         x.st(j, Disc{s < n ? (double)d[s] : 0.0, 0.0, 0.0});
       }
       __syncthreads();
-      dfft<false>(x, lg, tw);
+      dfft<false>(x, lg, tw, rw);
       if (op == 0) {
         for (int j = threadIdx.x; j < m; j += blockDim.x) A.st(j, x.ld(j));
       } else {  // P:210 pointwise, written bit-reversed for the inverse DIT
@@ -131,7 +140,7 @@ __global__ void __launch_bounds__(TH, 1)
       s_rad = 0ull;
     }
     __syncthreads();
-    dfft<true>(x, lg, tw);  // P:211 with omega^-1 = conj
+    dfft<true>(x, lg, tw, rw);  // P:211 with omega^-1 = conj
     // 1/m exact; certify c_i, i < 2n-1, snap into int32 coefficients
     const double sc = 1.0 / (double)m;
     int32_t cv[16];  // m / TH <= 16
@@ -165,15 +174,15 @@ __global__ void __launch_bounds__(TH, 1)
 
 }  // namespace dk
 
-int disc_smem(int lg) { return 24 << lg; }
+int disc_smem(int lg) { return (((20 << lg) + 15) & ~15) + (8 << lg) + 16; }  // state + m/2 twiddle centers
 
-int disc_launch(const uint8_t *a, const uint8_t *b, int n, int batch, int lg, const void *tw, void *scratch,
-                uint8_t *prod, uint8_t *cert, double *max_radius, int grid, cudaStream_t s) {
+int disc_launch(const uint8_t *a, const uint8_t *b, int n, int batch, int lg, const void *tw, double rw,
+                void *scratch, uint8_t *prod, uint8_t *cert, double *max_radius, int grid, cudaStream_t s) {
   const int smem = disc_smem(lg);
   if (cudaFuncSetAttribute(dk::disc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
     return -1;
-  dk::disc_kernel<<<grid, dk::TH, smem, s>>>(a, b, n, batch, lg, (const double4 *)tw, (double *)scratch, prod, cert,
-                                             max_radius);
+  dk::disc_kernel<<<grid, dk::TH, smem, s>>>(a, b, n, batch, lg, (const double2 *)tw, rw, (double *)scratch, prod,
+                                             cert, max_radius);
   return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
 }
 

@@ -85,8 +85,8 @@ int v3g_launch(int prec, int m, const KParams &kp, const GroupArgs &ga, int grid
 
 // circular containment sets, m <= 8192
 int disc_smem(int lg);
-int disc_launch(const uint8_t *a, const uint8_t *b, int n, int batch, int lg, const void *tw, void *scratch,
-                uint8_t *prod, uint8_t *cert, double *max_radius, int grid, cudaStream_t s);
+int disc_launch(const uint8_t *a, const uint8_t *b, int n, int batch, int lg, const void *tw, double rw,
+                void *scratch, uint8_t *prod, uint8_t *cert, double *max_radius, int grid, cudaStream_t s);
 // the naive (punctual, round-to-nearest) SS comparator
 int naive_smem(int lg, int prec);
 int naive_launch(int prec, const uint8_t *a, const uint8_t *b, int n, int batch, int lg, const void *w, void *scratch,

@@ -37,7 +37,11 @@ def test_disc_parity_with_oracle(ctx, n):
     assert np.array_equal(cert[margin], ref["cert"][margin])
     assert np.array_equal(prod[cert], exact[cert])
     assert not prod[~cert].any()
-    ratio = rad / np.maximum(ref["max_radius"], 1e-300)
+    # R15: the GPU keeps radii as binary32 rounded up, so a radius that is only
+    # the 2^-1000 subnormal guards (zero products) becomes the smallest binary32
+    # subnormal; radii are compared above a 1e-30 floor (certification needs r < 0.5)
+    floor = 1e-30
+    ratio = np.maximum(rad, floor) / np.maximum(ref["max_radius"], floor)
     assert (ratio <= 2.0).all(), (n, ratio.max())
     assert (ratio >= 0.25).all(), (n, ratio.min())  # not suspiciously tight either
 
