@@ -82,20 +82,49 @@ __device__ __forceinline__ int brev(int j, int lg) { return lg ? (int)(__brev((u
 // twiddle of butterfly j is omega_{2^{s+1}}^j = omega_m^{j m / 2^{s+1}}
 // tw: twiddle centers omega_m^j (j < m/2) in shared memory; rw: one radius
 // bound for all of them (the host's max over j)
+__device__ __forceinline__ void bfly(Disc &e, Disc &o, const double2 t, bool inv, double rw, double nw) {
+  const Disc w{t.x, inv ? -t.y : t.y, rw};
+  const Disc wo = dmul(w, o, nw, l1(o));
+  o = dsum(e, wo, true);
+  e = dsum(e, wo, false);
+}
+// Stages are done two at a time (one shared-memory round trip per pair): a
+// group of four elements i0 + {0, 1, 2, 3} half takes the butterflies
+// (i0, i1), (i2, i3) of stage s (twiddle index j) and then (i0, i2), (i1, i3) of
+// stage s + 1 (j, j + half) -- the same butterflies, in the same order per
+// element, as one stage at a time (the radius between the two stays binary64
+// instead of being stored as binary32: slightly tighter); an odd last stage
+// runs alone.
 template <bool INV>
 __device__ __forceinline__ void dfft(SDisc x, int lg, const double2 *tw, double rw) {
   const int m = 1 << lg;
   const double nw = ru_add(1.0, rw);
-  for (int s = 0; s < lg; s++) {
+  int s = 0;
+  for (; s + 1 < lg; s += 2) {
+    const int half = 1 << s, st0 = m >> (s + 1), st1 = m >> (s + 2);
+    for (int g = threadIdx.x; g < m / 4; g += blockDim.x) {
+      const int j = g & (half - 1), i0 = ((g >> s) << (s + 2)) + j;
+      Disc v0 = x.ld(i0), v1 = x.ld(i0 + half), v2 = x.ld(i0 + 2 * half), v3 = x.ld(i0 + 3 * half);
+      const double2 ta = tw[j * st0];
+      bfly(v0, v1, ta, INV, rw, nw);
+      bfly(v2, v3, ta, INV, rw, nw);
+      bfly(v0, v2, tw[j * st1], INV, rw, nw);
+      bfly(v1, v3, tw[(j + half) * st1], INV, rw, nw);
+      x.st(i0, v0);
+      x.st(i0 + half, v1);
+      x.st(i0 + 2 * half, v2);
+      x.st(i0 + 3 * half, v3);
+    }
+    __syncthreads();
+  }
+  if (s < lg) {  // odd lg: the last stage alone
     const int half = 1 << s, stride = m >> (s + 1);
     for (int b = threadIdx.x; b < m / 2; b += blockDim.x) {
-      const int j = b & (half - 1), i0 = ((b >> s) << (s + 1)) + j, i1 = i0 + half;
-      const double2 t = tw[j * stride];
-      const Disc w{t.x, INV ? -t.y : t.y, rw};
-      const Disc o = x.ld(i1), e = x.ld(i0);
-      const Disc wo = dmul(w, o, nw, l1(o));
-      x.st(i0, dsum(e, wo, false));
-      x.st(i1, dsum(e, wo, true));
+      const int j = b & (half - 1), i0 = ((b >> s) << (s + 1)) + j;
+      Disc e = x.ld(i0), o = x.ld(i0 + half);
+      bfly(e, o, tw[j * stride], INV, rw, nw);
+      x.st(i0, e);
+      x.st(i0 + half, o);
     }
     __syncthreads();
   }
