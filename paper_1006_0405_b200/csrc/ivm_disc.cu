@@ -88,46 +88,41 @@ __device__ __forceinline__ void bfly(Disc &e, Disc &o, const double2 t, bool inv
   o = dsum(e, wo, true);
   e = dsum(e, wo, false);
 }
-// Stages are done two at a time (one shared-memory round trip per pair): a
-// group of four elements i0 + {0, 1, 2, 3} half takes the butterflies
-// (i0, i1), (i2, i3) of stage s (twiddle index j) and then (i0, i2), (i1, i3) of
-// stage s + 1 (j, j + half) -- the same butterflies, in the same order per
-// element, as one stage at a time (the radius between the two stays binary64
-// instead of being stored as binary32: slightly tighter); an odd last stage
-// runs alone.
+// K stages per shared-memory round trip: a group of 2^K elements
+// i0 + q half (q < 2^K, half = 2^s) runs, for t = 0 .. K-1, the stage-(s + t)
+// butterflies (q, q + 2^t) with twiddle index (j + (q mod 2^t) half) m / 2^(s+t+1)
+// -- the same butterflies, in the same order per element, as one stage at a
+// time (the radii between them stay binary64 instead of being stored as
+// binary32: slightly tighter).  K = 3 while three stages remain, then 2 or 1.
+template <bool INV, int K>
+__device__ __forceinline__ void dstages(SDisc x, int m, int s, const double2 *tw, double rw, double nw) {
+  constexpr int E = 1 << K;
+  const int half = 1 << s;
+  for (int g = threadIdx.x; g < m / E; g += blockDim.x) {
+    const int j = g & (half - 1), i0 = ((g >> s) << (s + K)) + j;
+    Disc v[E];
+#pragma unroll
+    for (int q = 0; q < E; q++) v[q] = x.ld(i0 + q * half);
+#pragma unroll
+    for (int t = 0; t < K; t++) {
+      const int h = 1 << t, stride = m >> (s + t + 1);
+#pragma unroll
+      for (int q = 0; q < E; q++)
+        if ((q & h) == 0) bfly(v[q], v[q + h], tw[(j + (q & (h - 1)) * half) * stride], INV, rw, nw);
+    }
+#pragma unroll
+    for (int q = 0; q < E; q++) x.st(i0 + q * half, v[q]);
+  }
+  __syncthreads();
+}
 template <bool INV>
 __device__ __forceinline__ void dfft(SDisc x, int lg, const double2 *tw, double rw) {
   const int m = 1 << lg;
   const double nw = ru_add(1.0, rw);
   int s = 0;
-  for (; s + 1 < lg; s += 2) {
-    const int half = 1 << s, st0 = m >> (s + 1), st1 = m >> (s + 2);
-    for (int g = threadIdx.x; g < m / 4; g += blockDim.x) {
-      const int j = g & (half - 1), i0 = ((g >> s) << (s + 2)) + j;
-      Disc v0 = x.ld(i0), v1 = x.ld(i0 + half), v2 = x.ld(i0 + 2 * half), v3 = x.ld(i0 + 3 * half);
-      const double2 ta = tw[j * st0];
-      bfly(v0, v1, ta, INV, rw, nw);
-      bfly(v2, v3, ta, INV, rw, nw);
-      bfly(v0, v2, tw[j * st1], INV, rw, nw);
-      bfly(v1, v3, tw[(j + half) * st1], INV, rw, nw);
-      x.st(i0, v0);
-      x.st(i0 + half, v1);
-      x.st(i0 + 2 * half, v2);
-      x.st(i0 + 3 * half, v3);
-    }
-    __syncthreads();
-  }
-  if (s < lg) {  // odd lg: the last stage alone
-    const int half = 1 << s, stride = m >> (s + 1);
-    for (int b = threadIdx.x; b < m / 2; b += blockDim.x) {
-      const int j = b & (half - 1), i0 = ((b >> s) << (s + 1)) + j;
-      Disc e = x.ld(i0), o = x.ld(i0 + half);
-      bfly(e, o, tw[j * stride], INV, rw, nw);
-      x.st(i0, e);
-      x.st(i0 + half, o);
-    }
-    __syncthreads();
-  }
+  for (; s + 3 <= lg; s += 3) dstages<INV, 3>(x, m, s, tw, rw, nw);
+  if (lg - s == 2) dstages<INV, 2>(x, m, s, tw, rw, nw);
+  if (lg - s == 1) dstages<INV, 1>(x, m, s, tw, rw, nw);
 }
 
 __global__ void __launch_bounds__(TH, 1)
