@@ -14,9 +14,11 @@ code with the CUDA path (paper_1006_0405_b200/); the product never imports it.
 
 Parity status: every function here is pinned by ``tests/test_oracle_*.py``
 against values that do not come from this package (paper values, exact
-rationals, closed forms, Python int, brute force, mpmath DFTs), except the
-exact interval radii, which the paper does not print ("parity unpinned" for
-radius values).
+rationals, closed forms, Python int, brute force, mpmath DFTs).  The interval
+radii, which the paper does not print, are pinned by an independent
+exact-rational recomputation of whole small multiplications
+(tests/test_oracle_exact_ss.py: every output interval and the max radius,
+bit for bit).
 """
 from __future__ import annotations
 
@@ -69,6 +71,11 @@ def lib():
         L.oracle_fft_length.argtypes = [S]
         L.oracle_fft_length.restype = S
         L.oracle_certify_f64.argtypes = [P, S, P, P]
+        L.oracle_certify_f32.argtypes = [P, S, P, P]
+        L.oracle_max_radius_f64.argtypes = [P, S]
+        L.oracle_max_radius_f64.restype = ctypes.c_double
+        L.oracle_max_radius_f32.argtypes = [P, S]
+        L.oracle_max_radius_f32.restype = ctypes.c_double
         L.oracle_self_check.restype = I
         L.oracle_disc_batch.argtypes = [P, P, S, S, P, P, P, P, P, P, P, I]
         L.oracle_disc_batch.restype = I
@@ -230,13 +237,25 @@ def fft(x: np.ndarray, inverse: int = 0, prec: str = "f64") -> np.ndarray:
     return out
 
 
-def certify(iv: np.ndarray):
-    """P:24 rule on [len][4] binary64 intervals -> (coeff int64, flag bool)."""
-    iv = np.ascontiguousarray(iv, dtype=np.float64).reshape(-1, 4)
+def certify(iv: np.ndarray, prec: str = "f64"):
+    """P:24 rule on [len][4] intervals -> (coeff int64, flag bool).  The same C
+    function ss_multiply_* applies to its output (R8)."""
+    dt = np.float64 if prec == "f64" else np.float32
+    iv = np.ascontiguousarray(iv, dtype=dt).reshape(-1, 4)
     c = np.zeros(iv.shape[0], np.int64)
     f = np.zeros(iv.shape[0], np.uint8)
-    lib().oracle_certify_f64(_p(iv), iv.shape[0], _p(c), _p(f))
+    fn = lib().oracle_certify_f64 if prec == "f64" else lib().oracle_certify_f32
+    fn(_p(iv), iv.shape[0], _p(c), _p(f))
     return c, f.astype(bool)
+
+
+def max_radius(iv: np.ndarray, prec: str = "f64") -> float:
+    """DESIGN.md R10 radius over [len][4] intervals: max over both parts of
+    RU(hi - lo)/2 (NaN -> inf).  The same C function ss_multiply_* applies."""
+    dt = np.float64 if prec == "f64" else np.float32
+    iv = np.ascontiguousarray(iv, dtype=dt).reshape(-1, 4)
+    fn = lib().oracle_max_radius_f64 if prec == "f64" else lib().oracle_max_radius_f32
+    return float(fn(_p(iv), iv.shape[0]))
 
 
 def self_check() -> bool:

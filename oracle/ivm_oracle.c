@@ -118,6 +118,42 @@ void oracle_carry(const int64_t *v, size_t n, uint8_t *z) {
 }
 
 /* ------------------------------------------------------------------ */
+/* P:24 / P:247 round-and-certify and the radius (one definition each)  */
+/* ------------------------------------------------------------------ */
+
+/* P:24 "choose the unique integer in the containment set; if there are
+ * multiple, report an error" with DESIGN.md R8/R18: the real part [lo, hi]
+ * holds exactly one integer iff ceil(lo) == floor(hi); the imaginary part
+ * must hold only 0.  NaN never certifies (comparisons fail).
+ * Intervals are [len][4] binary64 (re.lo, re.hi, im.lo, im.hi).  Writes the
+ * unique integers to coeff (nullable; 0 where not certified) and returns the
+ * first failing index, or -1 if every entry certifies. */
+static int32_t certify_span(const double *iv, size_t len, int64_t *coeff) {
+    int32_t bad = -1;
+    for (size_t i = 0; i < len; i++) {
+        double cl = ceil(iv[4 * i]), fh = floor(iv[4 * i + 1]);
+        double il = ceil(iv[4 * i + 2]), ih = floor(iv[4 * i + 3]);
+        int unique = (cl == fh) && (il == 0.0) && (ih == 0.0);
+        if (coeff) coeff[i] = unique ? (int64_t)cl : 0;
+        if (!unique && bad < 0) bad = (int32_t)i;
+    }
+    return bad;
+}
+
+/* DESIGN.md R10: the radius of an interval is (hi - lo)/2, here rounded up
+ * (the caller is in FE_UPWARD; the halving is exact), NaN counted as +inf;
+ * the max is taken over both parts of every entry of [len][4]. */
+static double max_radius_span(const double *iv, size_t len) {
+    double rad = 0.0;
+    for (size_t i = 0; i < 2 * len; i++) {
+        double r = (iv[2 * i + 1] - iv[2 * i]) / 2.0;
+        if (r != r) r = INFINITY;
+        if (r > rad) rad = r;
+    }
+    return rad;
+}
+
+/* ------------------------------------------------------------------ */
 /* §2.5 interval arithmetic, instantiated for T = double and T = float  */
 /* ------------------------------------------------------------------ */
 
@@ -229,23 +265,20 @@ static int ss_multiply_##S(const uint8_t *a, const uint8_t *b, size_t n,       \
     for (size_t i = 0; i < N; i++) A[i] = cdivk_##S(A[i], (T)N); /* P:97 1/n */\
     if (intervals_out)                                                         \
         for (size_t i = 0; i < N; i++) store_##S(intervals_out + 4 * i, A[i]); \
-    /* P:24 / P:247: the unique integer in each containment set */             \
-    int ok = 1; int32_t bad = -1; double rad = 0.0;                            \
-    for (size_t i = 0; i + 1 < 2 * n; i++) {                                   \
-        civ_##S z = A[i];                                                      \
-        double rr = ((double)z.re.hi - (double)z.re.lo) / 2.0;                 \
-        double ri = ((double)z.im.hi - (double)z.im.lo) / 2.0;                 \
-        if (rr > rad || rr != rr) rad = (rr != rr) ? INFINITY : (rr > rad ? rr : rad); \
-        if (ri > rad || ri != ri) rad = (ri != ri) ? INFINITY : (ri > rad ? ri : rad); \
-        double cl = ceil((double)z.re.lo), fh = floor((double)z.re.hi);        \
-        double il = ceil((double)z.im.lo), ih = floor((double)z.im.hi);        \
-        int unique = (cl == fh) && (il == 0.0) && (ih == 0.0);                 \
-        if (!unique) { if (ok) bad = (int32_t)i; ok = 0; }                     \
-        else if (coeff) coeff[i] = (int64_t)cl;                                \
+    /* P:24 / P:247: the unique integer in each containment set, over the   */ \
+    /* 2n-1 used coefficients; the same two functions the pins call. */ \
+    size_t used = 2 * n - 1;                                                   \
+    double *ud = (double *)malloc(used * 4 * sizeof(double));                  \
+    for (size_t i = 0; i < used; i++) {    /* binary32 -> binary64 is exact */ \
+        ud[4 * i] = (double)A[i].re.lo; ud[4 * i + 1] = (double)A[i].re.hi;    \
+        ud[4 * i + 2] = (double)A[i].im.lo; ud[4 * i + 3] = (double)A[i].im.hi; \
     }                                                                          \
+    int32_t bad = certify_span(ud, used, coeff);                               \
+    int ok = bad < 0;                                                          \
+    double rad = max_radius_span(ud, used);                                    \
     if (ok) {                                                                  \
         int64_t *c = coeff ? coeff : (int64_t *)malloc((2 * n - 1) * sizeof(int64_t)); \
-        if (!coeff) for (size_t i = 0; i + 1 < 2 * n; i++) c[i] = (int64_t)ceil((double)A[i].re.lo); \
+        if (!coeff) certify_span(ud, used, c);                                 \
         oracle_carry(c, n, prod);                                /* P:229-235 */ \
         if (!coeff) free(c);                                                   \
     } else {                                                                   \
@@ -253,6 +286,7 @@ static int ss_multiply_##S(const uint8_t *a, const uint8_t *b, size_t n,       \
     }                                                                          \
     if (maxrad) *maxrad = rad;                                                 \
     if (first_bad) *first_bad = bad;                                           \
+    free(ud);                                                                  \
     free(ap); free(bp); free(A); free(Bv);                                     \
     return ok;                                                                 \
 }
@@ -315,16 +349,39 @@ int oracle_ivmul_batch(const uint8_t *a, const uint8_t *b, size_t n, size_t batc
     return 0;
 }
 
-/* P:24 / P:247 rule on its own (for the worked-example pins):
- * per [len][4] interval, flag 1 and coeff = the unique integer if the real
- * part holds exactly one integer and the imaginary part holds only 0. */
+/* P:24 / P:247 rule and the radius on their own (for the pins): the very
+ * functions ss_multiply_* calls.  iv: [len][4] (binary64, or binary32 for
+ * the _f32 twins, widened exactly); flag[i] = 1 and coeff[i] = the unique
+ * integer where entry i certifies. */
 void oracle_certify_f64(const double *iv, size_t len, int64_t *coeff, uint8_t *flag) {
     for (size_t i = 0; i < len; i++) {
-        double cl = ceil(iv[4 * i]), fh = floor(iv[4 * i + 1]);
-        double il = ceil(iv[4 * i + 2]), ih = floor(iv[4 * i + 3]);
-        flag[i] = (uint8_t)((cl == fh) && (il == 0.0) && (ih == 0.0));
-        coeff[i] = flag[i] ? (int64_t)cl : 0;
+        int64_t c;
+        flag[i] = (uint8_t)(certify_span(iv + 4 * i, 1, &c) < 0);
+        coeff[i] = c;
     }
+}
+void oracle_certify_f32(const float *iv, size_t len, int64_t *coeff, uint8_t *flag) {
+    for (size_t i = 0; i < len; i++) {
+        double d[4] = { iv[4 * i], iv[4 * i + 1], iv[4 * i + 2], iv[4 * i + 3] };
+        int64_t c;
+        flag[i] = (uint8_t)(certify_span(d, 1, &c) < 0);
+        coeff[i] = c;
+    }
+}
+double oracle_max_radius_f64(const double *iv, size_t len) {
+    int old = fegetround(); enter();
+    double r = max_radius_span(iv, len);
+    fesetround(old);
+    return r;
+}
+double oracle_max_radius_f32(const float *iv, size_t len) {
+    int old = fegetround(); enter();
+    double *d = (double *)malloc((len ? len : 1) * 4 * sizeof(double));
+    for (size_t i = 0; i < 4 * len; i++) d[i] = iv[i];
+    double r = max_radius_span(d, len);
+    free(d);
+    fesetround(old);
+    return r;
 }
 
 int oracle_max_threads(void) {

@@ -99,9 +99,10 @@ def test_cmul_contains_sampled_products():
         assert r[i, 2] == rd64(b1[0] + b2[0]) and r[i, 3] == ru64(b1[1] + b2[1])
 
 
-def test_certify_worked_examples():
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_certify_worked_examples(prec):
     for ex in GOLD["certify"]:
-        c, f = oracle.certify(np.array(ex["iv"], float))
+        c, f = oracle.certify(np.array(ex["iv"], float), prec)
         assert bool(f[0]) == ex["unique"], ex
         if ex["unique"]:
             assert c[0] == ex["value"]
