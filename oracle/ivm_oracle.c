@@ -128,7 +128,7 @@ void oracle_carry(const int64_t *v, size_t n, uint8_t *z) {
  * Intervals are [len][4] binary64 (re.lo, re.hi, im.lo, im.hi).  Writes the
  * unique integers to coeff (nullable; 0 where not certified) and returns the
  * first failing index, or -1 if every entry certifies. */
-static int32_t certify_span(const double *iv, size_t len, int64_t *coeff) {
+int32_t oracle_certify_span(const double *iv, size_t len, int64_t *coeff) {
     int32_t bad = -1;
     for (size_t i = 0; i < len; i++) {
         double cl = ceil(iv[4 * i]), fh = floor(iv[4 * i + 1]);
@@ -273,12 +273,12 @@ static int ss_multiply_##S(const uint8_t *a, const uint8_t *b, size_t n,       \
         ud[4 * i] = (double)A[i].re.lo; ud[4 * i + 1] = (double)A[i].re.hi;    \
         ud[4 * i + 2] = (double)A[i].im.lo; ud[4 * i + 3] = (double)A[i].im.hi; \
     }                                                                          \
-    int32_t bad = certify_span(ud, used, coeff);                               \
+    int32_t bad = oracle_certify_span(ud, used, coeff);                               \
     int ok = bad < 0;                                                          \
     double rad = max_radius_span(ud, used);                                    \
     if (ok) {                                                                  \
         int64_t *c = coeff ? coeff : (int64_t *)malloc((2 * n - 1) * sizeof(int64_t)); \
-        if (!coeff) certify_span(ud, used, c);                                 \
+        if (!coeff) oracle_certify_span(ud, used, c);                                 \
         oracle_carry(c, n, prod);                                /* P:229-235 */ \
         if (!coeff) free(c);                                                   \
     } else {                                                                   \
@@ -356,7 +356,7 @@ int oracle_ivmul_batch(const uint8_t *a, const uint8_t *b, size_t n, size_t batc
 void oracle_certify_f64(const double *iv, size_t len, int64_t *coeff, uint8_t *flag) {
     for (size_t i = 0; i < len; i++) {
         int64_t c;
-        flag[i] = (uint8_t)(certify_span(iv + 4 * i, 1, &c) < 0);
+        flag[i] = (uint8_t)(oracle_certify_span(iv + 4 * i, 1, &c) < 0);
         coeff[i] = c;
     }
 }
@@ -364,7 +364,7 @@ void oracle_certify_f32(const float *iv, size_t len, int64_t *coeff, uint8_t *fl
     for (size_t i = 0; i < len; i++) {
         double d[4] = { iv[4 * i], iv[4 * i + 1], iv[4 * i + 2], iv[4 * i + 3] };
         int64_t c;
-        flag[i] = (uint8_t)(certify_span(d, 1, &c) < 0);
+        flag[i] = (uint8_t)(oracle_certify_span(d, 1, &c) < 0);
         coeff[i] = c;
     }
 }

@@ -118,6 +118,9 @@ static size_t d_fft_len(size_t n) {
     return N;
 }
 
+/* ivm_oracle.c: the P:24 certify rule (one definition for both oracles) */
+int32_t oracle_certify_span(const double *iv, size_t len, int64_t *coeff);
+
 /* one multiplication (P:203-211 with discs); returns the certified flag */
 static int d_multiply(const uint8_t *a, const uint8_t *b, size_t n, const double *tw, size_t N,
                       uint8_t *prod, int64_t *coeff, double *maxrad, int32_t *first_bad, double *discs_out) {
@@ -135,28 +138,24 @@ static int d_multiply(const uint8_t *a, const uint8_t *b, size_t n, const double
         for (size_t i = 0; i < N; i++) {
             discs_out[3 * i] = A[i].cr; discs_out[3 * i + 1] = A[i].ci; discs_out[3 * i + 2] = A[i].r;
         }
-    int ok = 1;
-    int32_t bad = -1;
+    /* P:24 on the enclosing rectangle [cr - r, cr + r] + i[ci - r, ci + r]
+     * (rounded outward), by the rectangular oracle's certify function */
+    size_t used = 2 * n - 1;
+    double *box = (double *)malloc(used * 4 * sizeof(double));
     double rad = 0.0;
-    for (size_t i = 0; i + 1 < 2 * n; i++) {
+    for (size_t i = 0; i < used; i++) {
         disc z = A[i];
         if (z.r > rad || z.r != z.r) rad = (z.r != z.r) ? INFINITY : z.r;
-        double rl = -((-z.cr) + z.r), rh = z.cr + z.r;   /* RD(cr - r), RU(cr + r) */
-        double il = -((-z.ci) + z.r), ih = z.ci + z.r;
-        double cl = ceil(rl), fh = floor(rh);
-        int unique = (cl == fh) && (ceil(il) == 0.0) && (floor(ih) == 0.0);
-        if (!unique) { if (ok) bad = (int32_t)i; ok = 0; }
-        else if (coeff) coeff[i] = (int64_t)cl;
+        box[4 * i] = -((-z.cr) + z.r); box[4 * i + 1] = z.cr + z.r;   /* RD(cr - r), RU(cr + r) */
+        box[4 * i + 2] = -((-z.ci) + z.r); box[4 * i + 3] = z.ci + z.r;
     }
-    if (ok) {
-        int64_t *c = coeff ? coeff : (int64_t *)malloc((2 * n - 1) * sizeof(int64_t));
-        if (!coeff)
-            for (size_t i = 0; i + 1 < 2 * n; i++) c[i] = (int64_t)ceil(-((-A[i].cr) + A[i].r));
-        oracle_carry(c, n, prod);
-        if (!coeff) free(c);
-    } else {
-        memset(prod, 0, 2 * n);
-    }
+    int64_t *c = coeff ? coeff : (int64_t *)malloc(used * sizeof(int64_t));
+    int32_t bad = oracle_certify_span(box, used, c);
+    int ok = bad < 0;
+    if (ok) oracle_carry(c, n, prod);
+    else memset(prod, 0, 2 * n);
+    if (!coeff) free(c);
+    free(box);
     if (maxrad) *maxrad = rad;
     if (first_bad) *first_bad = bad;
     free(ap); free(bp); free(A); free(B);
