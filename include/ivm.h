@@ -35,7 +35,12 @@
  *     launch and write nothing; CUDA failures return IVM_ECUDA and are
  *     sticky for the context;
  *   - determinism: identical inputs give bitwise identical outputs;
- *   - thread safety: one host thread per context at a time.
+ *   - thread safety: one host thread per context at a time;
+ *   - streams: every call on a context uses the context's scratch buffers,
+ *     so calls on one context are ordered even across streams: a call on a
+ *     different stream than the previous call's first makes its stream wait
+ *     for the previous call's work (cudaStreamWaitEvent on an event the
+ *     previous call recorded).  Calls on distinct contexts run concurrently.
  */
 #ifndef IVM_H
 #define IVM_H
@@ -105,7 +110,10 @@ int ivm_multiply_batched(ivm_ctx_t ctx, const uint8_t *a, const uint8_t *b, size
  *                          the pair is certified);
  *   dump_pairs [n_dump]  : pair indices whose final coefficient intervals are
  *                          written to intervals [n_dump][m][4] as binary64
- *                          (re.lo, re.hi, im.lo, im.hi), m = ivm_fft_length(n). */
+ *                          (re.lo, re.hi, im.lo, im.hi), m = ivm_fft_length(n).
+ *                          The odd-frequency kernels (binary64 with m >= 64,
+ *                          binary32 with m >= 1024) compute each coefficient
+ *                          as a real interval: their im.lo / im.hi are NaN. */
 int ivm_multiply_batched_diag(ivm_ctx_t ctx, const uint8_t *a, const uint8_t *b, size_t n,
                               size_t batch, uint8_t *prod, uint8_t *certified, int prec,
                               void *cuda_stream, double *max_radius, int32_t *first_bad,

@@ -82,6 +82,7 @@ def lib():
         L.oracle_disc_op.argtypes = [I, P, P, P, S]
         L.oracle_disc_fft.argtypes = [P, P, P, S, I]
         L.oracle_max_threads.restype = I
+        L.oracle_residue_check_batch.argtypes = [P, P, P, S, S, P, I, P, I]
         _lib = L
     return _lib
 
@@ -192,6 +193,59 @@ def coefficients(a: np.ndarray, b: np.ndarray, nthreads: int = 0) -> np.ndarray:
     z = np.zeros((B, 2 * n - 1), np.int64)
     lib().oracle_coefficients_batch(_p(a), _p(b), n, B, _p(z), nthreads)
     return z
+
+
+def _is_prime(p: int) -> bool:
+    """Deterministic Miller-Rabin for p < 3.3e24 (bases: the first 12 primes)."""
+    if p < 2:
+        return False
+    small = [2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37]
+    for q in small:
+        if p % q == 0:
+            return p == q
+    d, s = p - 1, 0
+    while d % 2 == 0:
+        d, s = d // 2, s + 1
+    for a in small:
+        x = pow(a, d, p)
+        if x in (1, p - 1):
+            continue
+        for _ in range(s - 1):
+            x = x * x % p
+            if x == p - 1:
+                break
+        else:
+            return False
+    return True
+
+
+def random_primes(k: int = 2, bits: int = 61, seed: int | None = None) -> list[int]:
+    """k distinct random primes of `bits` bits (the residue check's moduli)."""
+    import random
+    rng = random.Random(seed)
+    out = []
+    while len(out) < k:
+        p = rng.getrandbits(bits) | (1 << (bits - 1)) | 1
+        if p not in out and _is_prime(p):
+            out.append(p)
+    return out
+
+
+def residue_check(a: np.ndarray, b: np.ndarray, z: np.ndarray, primes=None, nthreads: int = 0) -> np.ndarray:
+    """per pair, True iff z == a*b modulo every prime in `primes`
+    (default: two fresh random 61-bit primes).  [B][n], [B][n], [B][2n]."""
+    a = np.ascontiguousarray(a, dtype=np.uint8)
+    b = np.ascontiguousarray(b, dtype=np.uint8)
+    z = np.ascontiguousarray(z, dtype=np.uint8)
+    if a.ndim == 1:
+        a, b, z = a[None], b[None], z[None]
+    B, n = a.shape
+    assert b.shape == (B, n) and z.shape == (B, 2 * n)
+    pr = np.array(primes if primes is not None else random_primes(2), np.uint64)
+    assert all(0 < int(p) < 2 ** 62 for p in pr)
+    ok = np.zeros(B, np.uint8)
+    lib().oracle_residue_check_batch(_p(a), _p(b), _p(z), n, B, _p(pr), len(pr), _p(ok), nthreads)
+    return ok.astype(bool)
 
 
 def carry(coeffs: np.ndarray) -> np.ndarray:

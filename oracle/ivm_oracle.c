@@ -415,6 +415,45 @@ void oracle_coefficients_batch(const uint8_t *a, const uint8_t *b, size_t n, siz
         oracle_coefficients(a + (size_t)p * n, n, b + (size_t)p * n, n, z + (size_t)p * (2 * n - 1));
 }
 
+/* S:432 "residues modulo 61-bit primes": a product z (2n digits) of x, y
+ * (n digits each) is checked as (x mod p)(y mod p) == z mod p for each given
+ * modulus p < 2^62 (primes, drawn by the caller).  Horner's rule over the
+ * base-256 digits, most significant first, seven digits per reduction.
+ * ok[pair] = 1 iff every modulus agrees.  A wrong product passes one random
+ * 61-bit prime with probability < 2^-40 at these sizes (a nonzero difference
+ * below 2^(16 n) has at most 16n/60 prime factors of 61 bits). */
+static uint64_t mod_digits(const uint8_t *d, size_t len, uint64_t p) {
+    unsigned __int128 r = 0;
+    size_t i = len;
+    while (i > 0) {
+        size_t k = i >= 7 ? 7 : i;
+        i -= k;
+        uint64_t chunk = 0;
+        for (size_t j = k; j-- > 0;) chunk = (chunk << 8) | d[i + j];
+        r = ((r << (8 * k)) + chunk) % p;
+    }
+    return (uint64_t)r;
+}
+
+void oracle_residue_check_batch(const uint8_t *a, const uint8_t *b, const uint8_t *z, size_t n, size_t batch,
+                                const uint64_t *primes, int nprimes, uint8_t *ok, int nthreads) {
+    (void)nthreads;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 16)
+#endif
+    for (long long q = 0; q < (long long)batch; q++) {
+        int good = 1;
+        for (int k = 0; k < nprimes; k++) {
+            uint64_t p = primes[k];
+            unsigned __int128 xy = (unsigned __int128)mod_digits(a + (size_t)q * n, n, p) *
+                                   mod_digits(b + (size_t)q * n, n, p);
+            if ((uint64_t)(xy % p) != mod_digits(z + (size_t)q * 2 * n, 2 * n, p)) good = 0;
+        }
+        ok[q] = (uint8_t)good;
+    }
+}
+
 /* --- single steps, for the pins (each one operation of §2.5 / §2.2) --- */
 
 /* op: 0 add, 1 sub, 2 mul; vectors of [len][2] */

@@ -104,6 +104,37 @@ def _ptr(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
+def _check_operands(a, b, on_device: bool, device: int | None = None):
+    """Every wrapper's operand check: uint8, same shape [batch][n] (or [n]),
+    contiguous, and on the context's CUDA device (on_device) or in host memory
+    (the host entry point).  The C ABI reads a and b as dense [batch][n] rows,
+    so anything else would multiply the wrong digits."""
+    import torch
+    for name, t in (("a", a), ("b", b)):
+        if not isinstance(t, torch.Tensor) or t.dtype != torch.uint8:
+            raise TypeError(f"{name} must be a torch.uint8 tensor")
+        if t.dim() not in (1, 2) or t.numel() == 0:
+            raise ValueError(f"{name} must be a non-empty [batch][n] (or [n]) tensor")
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous (row-major [batch][n])")
+        if on_device:
+            if not t.is_cuda or (device is not None and t.device.index != device):
+                raise ValueError(f"{name} must be a CUDA tensor on cuda:{device}")
+        elif t.is_cuda:
+            raise ValueError(f"{name} must be a host tensor for the host entry point")
+    if a.shape != b.shape:
+        raise ValueError(f"operand shapes differ: {tuple(a.shape)} vs {tuple(b.shape)} "
+                         "(zero-pad the shorter operand)")
+
+
+def _check_out(t, shape, dtype, on_device: bool, name: str):
+    import torch
+    if not isinstance(t, torch.Tensor) or t.dtype != dtype or tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must be a {dtype} tensor of shape {tuple(shape)}")
+    if not t.is_contiguous() or t.is_cuda != on_device:
+        raise ValueError(f"{name} must be contiguous and {'on the device' if on_device else 'in host memory'}")
+
+
 def _stream(stream):
     import torch
     if stream is None:
@@ -142,16 +173,17 @@ class Context:
     def multiply(self, a, b, prec: int = F64, out=None, cert=None, stream=None):
         """Batched multiply of uint8 CUDA tensors a, b [batch][n] (or [n])."""
         import torch
+        _check_operands(a, b, True, self.device)
         squeeze = a.dim() == 1
         if squeeze:
             a, b = a[None], b[None]
-        assert a.dtype == torch.uint8 and b.dtype == torch.uint8 and a.shape == b.shape
-        assert a.is_cuda and b.is_cuda and a.is_contiguous() and b.is_contiguous()
         B, n = a.shape
         if out is None:
             out = torch.empty((B, 2 * n), dtype=torch.uint8, device=a.device)
         if cert is None:
             cert = torch.empty((B,), dtype=torch.uint8, device=a.device)
+        _check_out(out, (B, 2 * n), torch.uint8, True, "out")
+        _check_out(cert, (B,), torch.uint8, True, "cert")
         _check(lib().ivm_multiply_batched(self._h, _ptr(a), _ptr(b), n, B, _ptr(out), _ptr(cert),
                                           prec, _stream(stream)), "ivm_multiply_batched")
         if squeeze:
@@ -161,6 +193,9 @@ class Context:
     def multiply_diag(self, a, b, prec: int = F64, dump_pairs=None, stream=None, coeffs=True):
         """Multiply with diagnostics: returns dict of CUDA tensors."""
         import torch
+        _check_operands(a, b, True, self.device)
+        if a.dim() == 1:
+            a, b = a[None], b[None]
         B, n = a.shape
         dev = a.device
         m = fft_length(n)
@@ -185,9 +220,13 @@ class Context:
         """The paper's naive (punctual, round-to-nearest) SS: [B][2n] u8,
         NOT guaranteed correct."""
         import torch
+        _check_operands(a, b, True, self.device)
+        if a.dim() == 1:
+            a, b = a[None], b[None]
         B, n = a.shape
         if out is None:
             out = torch.empty((B, 2 * n), dtype=torch.uint8, device=a.device)
+        _check_out(out, (B, 2 * n), torch.uint8, True, "out")
         _check(lib().ivm_multiply_naive(self._h, _ptr(a), _ptr(b), n, B, _ptr(out), prec, _stream(stream)),
                "ivm_multiply_naive")
         return out
@@ -196,11 +235,16 @@ class Context:
         """Circular containment sets (R15), fp64, n <= 4096:
         (products [B][2n] u8, certified [B] u8, max disc radius [B] f64 or None)."""
         import torch
+        _check_operands(a, b, True, self.device)
+        if a.dim() == 1:
+            a, b = a[None], b[None]
         B, n = a.shape
         if out is None:
             out = torch.empty((B, 2 * n), dtype=torch.uint8, device=a.device)
         if cert is None:
             cert = torch.empty((B,), dtype=torch.uint8, device=a.device)
+        _check_out(out, (B, 2 * n), torch.uint8, True, "out")
+        _check_out(cert, (B,), torch.uint8, True, "cert")
         rad = torch.empty((B,), dtype=torch.float64, device=a.device) if want_radius else None
         _check(lib().ivm_multiply_disc(self._h, _ptr(a), _ptr(b), n, B, _ptr(out), _ptr(cert), _ptr(rad),
                                        _stream(stream)), "ivm_multiply_disc")
@@ -209,9 +253,13 @@ class Context:
     def long_multiply(self, a, b, out=None, stream=None):
         """Exact long multiplication on the device: [B][2n] u8."""
         import torch
+        _check_operands(a, b, True, self.device)
+        if a.dim() == 1:
+            a, b = a[None], b[None]
         B, n = a.shape
         if out is None:
             out = torch.empty((B, 2 * n), dtype=torch.uint8, device=a.device)
+        _check_out(out, (B, 2 * n), torch.uint8, True, "out")
         _check(lib().ivm_long_multiply_batched(self._h, _ptr(a), _ptr(b), n, B, _ptr(out), _stream(stream)),
                "ivm_long_multiply_batched")
         return out
@@ -222,23 +270,35 @@ class Context:
         m = 64); returns (products [B][2n] u8, method [B] u8:
         1 fp32 interval, 2 fp64 interval, 3 long multiplication)."""
         import torch
+        _check_operands(a, b, True, self.device)
+        if a.dim() == 1:
+            a, b = a[None], b[None]
         B, n = a.shape
         if out is None:
             out = torch.empty((B, 2 * n), dtype=torch.uint8, device=a.device)
         if method is None:
             method = torch.empty((B,), dtype=torch.uint8, device=a.device)
+        _check_out(out, (B, 2 * n), torch.uint8, True, "out")
+        _check_out(method, (B,), torch.uint8, True, "method")
         _check(lib().ivm_multiply_exact(self._h, _ptr(a), _ptr(b), n, B, _ptr(out), _ptr(method), policy,
                                         _stream(stream)), "ivm_multiply_exact")
         return out, method
 
     def multiply_host(self, a, b, prec: int = F64, out=None, cert=None, stream=None):
-        """End-to-end path: host (pinned) uint8 tensors in, host tensors out."""
+        """End-to-end path: host uint8 tensors in (pinned for asynchronous
+        copies; pageable memory works but is copied synchronously), host
+        tensors out."""
         import torch
+        _check_operands(a, b, False)
+        if a.dim() == 1:
+            a, b = a[None], b[None]
         B, n = a.shape
         if out is None:
             out = torch.empty((B, 2 * n), dtype=torch.uint8, pin_memory=True)
         if cert is None:
             cert = torch.empty((B,), dtype=torch.uint8, pin_memory=True)
+        _check_out(out, (B, 2 * n), torch.uint8, False, "out")
+        _check_out(cert, (B,), torch.uint8, False, "cert")
         _check(lib().ivm_multiply_batched_host(self._h, _ptr(a), _ptr(b), n, B, _ptr(out),
                                                _ptr(cert), prec, _stream(stream)),
                "ivm_multiply_batched_host")

@@ -27,7 +27,6 @@ struct ivm_ctx {
   std::map<std::pair<int, int>, ivm::LaunchInfo> info3;
   bool force_v1 = false;
   bool force_v5 = false;   // IVM_KERNEL=v5: the group kernel also for m = 2^14 .. 2^16
-  bool force_v3g = false;  // IVM_KERNEL=v3g: the older global-state group kernel for every m >= 2^14
   std::map<std::pair<int, int>, void *> tw4;  // (log2m, prec) -> v4 role tables
   std::map<std::pair<int, int>, ivm::LaunchInfo> info4;
   std::map<std::pair<int, int>, void *> twn;  // (log2m, prec) -> round-to-nearest twiddles (naive SS)
@@ -51,12 +50,35 @@ struct ivm_ctx {
   // host API pipeline: copy-in / copy-out streams and per-chunk events
   cudaStream_t s_in = nullptr, s_out = nullptr;
   std::vector<cudaEvent_t> ev;
+  // the scratch buffers above are shared by every call on the context: a call
+  // on another stream than the previous call's waits for the previous call
+  cudaEvent_t done_ev = nullptr;
+  cudaStream_t last_stream = nullptr;
+  bool have_last = false;
 };
 
 static int cuda_fail(ivm_ctx_t c) {
   if (c) c->sticky = IVM_ECUDA;
   return IVM_ECUDA;
 }
+
+// Orders the calls of one context across streams (include/ivm.h "Streams"):
+// the guard makes the call's stream wait for the previous call's work when the
+// stream changed, and records the call's completion event when it returns.
+struct StreamOrder {
+  ivm_ctx_t c;
+  cudaStream_t s;
+  bool ok = true;
+  StreamOrder(ivm_ctx_t c_, void *stream) : c(c_), s((cudaStream_t)stream) {
+    if (c->have_last && c->last_stream != s) ok = cudaStreamWaitEvent(s, c->done_ev, 0) == cudaSuccess;
+  }
+  ~StreamOrder() {
+    if (cudaEventRecord(c->done_ev, s) == cudaSuccess) {
+      c->last_stream = s;
+      c->have_last = true;
+    }
+  }
+};
 
 static int log2m_for(size_t n) {
   if (n <= 1) return 0;
@@ -88,7 +110,7 @@ const char *ivm_strerror(int s) {
 
 size_t ivm_max_digits(int prec) {
   if (prec != IVM_F64 && prec != IVM_F32) return 0;
-  return ((size_t)1 << kMaxLog2M) / 2;  // 2n-1 <= 2^13
+  return ((size_t)1 << kMaxLog2M) / 2;  // 2n-1 <= m = 2^18
 }
 
 size_t ivm_fft_length(size_t n) { return n == 0 ? 0 : (size_t)1 << log2m_for(n); }
@@ -132,8 +154,11 @@ int ivm_create(ivm_ctx_t *ctx, int device) {
   }
   const char *kv = getenv("IVM_KERNEL");
   c->force_v1 = kv && strcmp(kv, "v1") == 0;
-  c->force_v3g = kv && strcmp(kv, "v3g") == 0;
   c->force_v5 = kv && strcmp(kv, "v5") == 0;
+  if (cudaEventCreateWithFlags(&c->done_ev, cudaEventDisableTiming) != cudaSuccess) {
+    delete c;
+    return IVM_ECUDA;
+  }
   c->consts = true;
   *ctx = c;
   return IVM_OK;
@@ -157,6 +182,7 @@ int ivm_destroy(ivm_ctx_t c) {
   if (c->s_in) cudaStreamDestroy(c->s_in);
   if (c->s_out) cudaStreamDestroy(c->s_out);
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+  if (c->done_ev) cudaEventDestroy(c->done_ev);
   delete c;
   return IVM_OK;
 }
@@ -186,9 +212,8 @@ static bool use_v3(ivm_ctx_t c, int m) { return !c->force_v1 && m >= 10 && m <= 
 // fp64 only: at fp32 (C4, the precision-limit sweep) the v1 kernel's full-interval
 // twiddles give ~2x tighter enclosures (93 % vs 0 % of 32-digit uniform pairs certified)
 static bool use_v6(ivm_ctx_t c, int m, int prec) { return !c->force_v1 && prec == IVM_F64 && m >= 6 && m <= 9; }
-static bool use_v4(ivm_ctx_t c, int m) { return !c->force_v3g && !c->force_v5 && m >= 14 && m <= 16; }
-static bool use_v5(ivm_ctx_t c, int m) { return !c->force_v3g && m >= 14 && m <= 18 && !use_v4(c, m); }
-static bool use_v3g(ivm_ctx_t c, int m) { return m >= 14 && m <= 18 && !use_v4(c, m) && !use_v5(c, m); }
+static bool use_v4(ivm_ctx_t c, int m) { return !c->force_v5 && m >= 14 && m <= 16; }
+static bool use_v5(ivm_ctx_t c, int m) { return m >= 14 && m <= 18 && !use_v4(c, m); }
 
 static int get_info5(ivm_ctx_t c, int m, int prec, ivm::LaunchInfo *li) {
   auto key = std::make_pair(m + 100, prec);
@@ -244,7 +269,7 @@ static int get_info4(ivm_ctx_t c, int m, int prec, ivm::LaunchInfo *li) {
 }
 
 static int get_table3(ivm_ctx_t c, int m, int prec, const void **out) {
-  const int radix = (m >= 6 && m <= 13) ? 8 : 16;  // v6 / v3 radix-8 plans; v3g radix 16
+  const int radix = 8;  // v6 / v3 radix-8 plans
   auto key = std::make_pair(m * 100 + radix, prec);
   auto it = c->tw3.find(key);
   if (it != c->tw3.end()) {
@@ -369,10 +394,6 @@ int ivm_reserve(ivm_ctx_t c, size_t n, size_t batch, int prec) {
     if (!r) r = get_info5(c, m, prec, &li);
     return r;
   }
-  if (use_v3g(c, m)) {
-    const void *t3;
-    return get_table3(c, m, prec, &t3);
-  }
   const void *t;
   ivm::LaunchInfo li;
   int r;
@@ -398,6 +419,8 @@ int ivm_multiply_batched_diag(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, s
   if (r) return r;
   if (n_dump && (!dump_pairs || !intervals)) return IVM_EINVAL;
   if (cudaSetDevice(c->device) != cudaSuccess) return cuda_fail(c);
+  StreamOrder order(c, stream);
+  if (!order.ok) return cuda_fail(c);
   cudaStream_t s = (cudaStream_t)stream;
   ivm::KParams kp{};
   kp.a = a; kp.b = b; kp.prod = prod; kp.cert = cert;
@@ -492,41 +515,6 @@ int ivm_multiply_batched_diag(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, s
     c->last_launches = launches + 1;
     return IVM_OK;
   }
-  if (use_v3g(c, m)) {
-    const void *tw;
-    r = get_table3(c, m, prec, &tw);
-    if (r) return r;
-    ivm::GroupInfo gi;
-    if (ivm::v3g_info(prec, m, &gi) != 0 || gi.blocks_per_sm < 1) return cuda_fail(c);
-    size_t groups = (size_t)c->sms * gi.blocks_per_sm / gi.C;
-    if (groups > batch) groups = batch;
-    if (groups < 1) return IVM_EUNSUPPORTED;
-    const size_t al = 256;
-    auto up = [&](size_t x) { return (x + al - 1) / al * al; };
-    const size_t b_state = up(groups * gi.state_bytes_per_group), b_coef = up(groups * gi.coef_bytes_per_group);
-    const size_t b_cert = up(groups * 16), b_agg = up(groups * gi.C * 4), b_ctr = up(groups * 4);
-    const size_t need = b_state + b_coef + b_cert + b_agg + b_ctr;
-    if (c->gscratch_bytes < need) {
-      cudaFree(c->gscratch);
-      c->gscratch = nullptr;
-      c->gscratch_bytes = 0;
-      if (cudaMalloc(&c->gscratch, need) != cudaSuccess) return IVM_ENOMEM;
-      c->gscratch_bytes = need;
-    }
-    char *g = (char *)c->gscratch;
-    ivm::GroupArgs ga;
-    ga.state = g;
-    ga.coef = (long long *)(g + b_state);
-    ga.cert = (int *)(g + b_state + b_coef);
-    ga.agg = (unsigned *)(g + b_state + b_coef + b_cert);
-    ga.ctr = (unsigned *)(g + b_state + b_coef + b_cert + b_agg);
-    ga.C = gi.C;
-    if (cudaMemsetAsync(ga.ctr, 0, b_ctr, s) != cudaSuccess) return cuda_fail(c);
-    kp.tw = tw;
-    if (ivm::v3g_launch(prec, m, kp, ga, (int)(groups * gi.C), s) != 0) return cuda_fail(c);
-    c->last_launches = launches + 1;
-    return IVM_OK;
-  }
   const void *tw;
   ivm::LaunchInfo li;
   const bool v3 = use_v3(c, m);
@@ -569,6 +557,8 @@ int ivm_multiply_batched_host(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, s
   int r = check_args(c, a, b, n, batch, prod, cert, prec);
   if (r) return r;
   if (cudaSetDevice(c->device) != cudaSuccess) return cuda_fail(c);
+  StreamOrder order(c, stream);
+  if (!order.ok) return cuda_fail(c);
   const size_t in = n * batch, out = 2 * n * batch;
   const size_t need = 2 * in + out + batch;
   if (c->stage_bytes < need) {
@@ -679,6 +669,8 @@ int ivm_long_multiply_batched(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, s
   if (n > kLongMaxDigits || batch > (size_t)0x7fffffff) return IVM_EUNSUPPORTED;
   if (c->sticky) return c->sticky;
   if (cudaSetDevice(c->device) != cudaSuccess) return cuda_fail(c);
+  StreamOrder order(c, stream);
+  if (!order.ok) return cuda_fail(c);
   int r = ensure_lscratch(c, long_chunk(n, batch) * (2 * n - 1) * 8);
   if (r) return r;
   int launches = 0;
@@ -693,6 +685,8 @@ int ivm_multiply_exact(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, size_t n
   if (n > kLongMaxDigits || batch > (size_t)0x7fffffff) return IVM_EUNSUPPORTED;
   if (c->sticky) return c->sticky;
   if (cudaSetDevice(c->device) != cudaSuccess) return cuda_fail(c);
+  StreamOrder order(c, stream);
+  if (!order.ok) return cuda_fail(c);
   cudaStream_t s = (cudaStream_t)stream;
   const size_t al = 256;
   auto up = [&](size_t x) { return (x + al - 1) / al * al; };
@@ -770,6 +764,8 @@ int ivm_multiply_naive(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, size_t n
   if (n > 4096 || batch > (size_t)0x7fffffff) return IVM_EUNSUPPORTED;
   if (c->sticky) return c->sticky;
   if (cudaSetDevice(c->device) != cudaSuccess) return cuda_fail(c);
+  StreamOrder order(c, stream);
+  if (!order.ok) return cuda_fail(c);
   const int lg = log2m_for(n) < 1 ? 1 : log2m_for(n);
   auto key = std::make_pair(lg, prec);
   void *w = nullptr;
@@ -781,7 +777,10 @@ int ivm_multiply_naive(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, size_t n
     std::vector<unsigned char> h(bytes);
     if (ivm::plan_twiddles_rn(lg, prec, h.data()) != 0) return IVM_EUNSUPPORTED;
     if (cudaMalloc(&w, bytes) != cudaSuccess) return IVM_ENOMEM;
-    if (cudaMemcpy(w, h.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess) return cuda_fail(c);
+    if (cudaMemcpy(w, h.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
+      cudaFree(w);
+      return cuda_fail(c);
+    }
     c->twn[key] = w;
   }
   const int smem = ivm::naive_smem(lg, prec);
@@ -807,6 +806,8 @@ int ivm_multiply_disc(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, size_t n,
   if (n > 4096 || batch > (size_t)0x7fffffff) return IVM_EUNSUPPORTED;
   if (c->sticky) return c->sticky;
   if (cudaSetDevice(c->device) != cudaSuccess) return cuda_fail(c);
+  StreamOrder order(c, stream);
+  if (!order.ok) return cuda_fail(c);
   const int lg = log2m_for(n);  // n = 1: m = 1 (no FFT stage)
   void *w = nullptr;
   double rw = 0.0;
@@ -826,8 +827,10 @@ int ivm_multiply_disc(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, size_t n,
       rw = r > rw ? r : rw;
     }
     if (cudaMalloc(&w, h.size() * sizeof(double)) != cudaSuccess) return IVM_ENOMEM;
-    if (cudaMemcpy(w, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
+    if (cudaMemcpy(w, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) {
+      cudaFree(w);
       return cuda_fail(c);
+    }
     c->twd[lg] = std::make_pair(w, rw);
   }
   size_t grid = (size_t)c->sms;

@@ -48,22 +48,6 @@ int v3_launch(int prec, int m, int radix, const KParams &kp, int grid, cudaStrea
 // small m (2^6 .. 2^9): 8192/m multiplications per 512-thread CTA
 int v6_info(int prec, int m, LaunchInfo *li);
 int v6_launch(int prec, int m, const KParams &kp, int grid, cudaStream_t s);
-// large m (2^14 .. 2^18): one group of C co-resident CTAs per multiplication
-struct GroupInfo {
-  int blocks_per_sm;
-  int C;
-  size_t state_bytes_per_group;
-  size_t coef_bytes_per_group;
-};
-struct GroupArgs {
-  unsigned *ctr;
-  int C;
-  void *state;
-  long long *coef;
-  int *cert;
-  unsigned *agg;
-};
-int v3g_info(int prec, int m, GroupInfo *gi);
 // m = 2^14 .. 2^16: one thread-block cluster of m/8192 CTAs per multiplication
 int upload_w64_v4(const double *w64, const float *w32);
 int v4_table_entries(int m);
@@ -81,7 +65,6 @@ struct Group5Args {
 int upload_w64_v5(const double *w64, const float *w32);
 int v5_info(int prec, int m, LaunchInfo *li);
 int v5_launch(int prec, int m, const KParams &kp, const Group5Args &ga, int groups, cudaStream_t s);
-int v3g_launch(int prec, int m, const KParams &kp, const GroupArgs &ga, int grid, cudaStream_t s);
 
 // circular containment sets, m <= 8192
 int disc_smem(int lg);

@@ -8,7 +8,6 @@
 #include "ivm_internal.h"
 #include "ivm_carry.cuh"
 #include "ivm_v3.cuh"
-#include "ivm_v3g.cuh"
 #include "ivm_v6.cuh"
 #include "ivm_twc_host.h"
 
@@ -143,45 +142,6 @@ int v3_launch(int prec, int m, int radix, const KParams &kp, int grid, cudaStrea
 }
 
 
-
-// ---- large m: group kernel (cooperative) ----
-template <typename T, int M> static int v3g_info_impl(GroupInfo *gi) {
-  auto k = v3::ivm_v3g_kernel<T, M>;
-  int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, 256, 0) != cudaSuccess) return -1;
-  gi->blocks_per_sm = nb;
-  gi->C = (1 << M) / 8192 < 1 ? 1 : (1 << M) / 8192;
-  gi->state_bytes_per_group = (size_t)6 * ((1 << M) / 2) * 2 * sizeof(T);
-  gi->coef_bytes_per_group = (size_t)(1 << M) * 8;
-  return 0;
-}
-template <int M> static int v3g_info_m(int prec, GroupInfo *gi) {
-  if constexpr (M < 14) {
-    return -4;
-  } else {
-    return prec == 0 ? v3g_info_impl<double, M>(gi) : v3g_info_impl<float, M>(gi);
-  }
-}
-int v3g_info(int prec, int m, GroupInfo *gi) { IVM_V3_DISPATCH(v3g_info_m, prec, gi) }
-
-template <int M> static int v3g_launch_m(int prec, const KParams &kp, const GroupArgs &ga, int grid, cudaStream_t s) {
-  if constexpr (M < 14) {
-    return -4;
-  } else {
-    v3::GroupCtx gc{ga.ctr, ga.C, ga.state, ga.coef, ga.cert, ga.agg};
-    KParams k2 = kp;
-    void *args[] = {(void *)&k2, (void *)&gc};
-    cudaError_t e;
-    if (prec == 0)
-      e = cudaLaunchCooperativeKernel((const void *)v3::ivm_v3g_kernel<double, M>, dim3(grid), dim3(256), args, 0, s);
-    else
-      e = cudaLaunchCooperativeKernel((const void *)v3::ivm_v3g_kernel<float, M>, dim3(grid), dim3(256), args, 0, s);
-    return e == cudaSuccess ? 0 : -1;
-  }
-}
-int v3g_launch(int prec, int m, const KParams &kp, const GroupArgs &ga, int grid, cudaStream_t s) {
-  IVM_V3_DISPATCH(v3g_launch_m, prec, kp, ga, grid, s)
-}
 
 // ---- small m (2^6 .. 2^9): one multiplication per m/16 lanes ----
 template <typename T, int M> static int v6_info_impl(LaunchInfo *li) {

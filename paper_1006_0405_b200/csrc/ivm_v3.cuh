@@ -420,7 +420,13 @@ struct CertAcc {  // per-thread; reduced once per multiplication
 // use int64 destinations (v5)
 template <typename T, typename D>
 __device__ __forceinline__ void certify_real(T lo, T hi, int i, int n, D *dst, CertAcc &acc, double *dump) {
-  if (dump) reinterpret_cast<double4 *>(dump)[i] = make_double4((double)lo, (double)hi, 0.0, 0.0);
+  // the odd-frequency kernels compute each coefficient as a REAL containment
+  // interval (R13): the imaginary slots of the dump are NaN ("not
+  // computed"), never a synthetic [0, 0]
+  if (dump) {
+    const double qnan = __longlong_as_double(0x7ff8000000000000LL);
+    reinterpret_cast<double4 *>(dump)[i] = make_double4((double)lo, (double)hi, qnan, qnan);
+  }
   if (i >= 2 * n - 1) return;
   const double l = (double)lo, h = (double)hi;
   const double cl = ceil(l);

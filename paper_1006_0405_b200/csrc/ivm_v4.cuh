@@ -92,10 +92,12 @@ __device__ __forceinline__ unsigned cluster_rank() {
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-// split barrier: arrive (no memory ordering: the remote reads it guards have
-// been consumed) now, wait later
-__device__ __forceinline__ void cluster_arrive_relaxed() {
-  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+// split barrier: arrive now, wait later.  The arrive has release semantics:
+// it orders this CTA's remote DSMEM reads before the other CTAs' writes that
+// follow their wait (write-after-read across the cluster; the PTX memory model
+// gives .relaxed no such ordering).
+__device__ __forceinline__ void cluster_arrive_release() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 __device__ __forceinline__ unsigned dsm_map(const void *p, unsigned cta) {
@@ -513,7 +515,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
     // (5) remote state / coefficient / chunk-bit reads done before the next pair
     // overwrites them: arrive now, wait just before the next state write (and
     // the next forward-last table, which replaces the coefficients)
-    cluster_arrive_relaxed();
+    cluster_arrive_release();
   }
   if (it > 0) cluster_wait();  // no CTA leaves while its shared memory may still be read
 }

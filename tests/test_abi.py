@@ -82,3 +82,26 @@ def test_max_digits():
     assert ivm.max_digits(ivm.F64) >= 4096
     assert ivm.max_digits(ivm.F32) >= 256
     assert ivm.lib().ivm_max_digits(9) == 0
+
+
+def test_binding_operand_checks():
+    """Every wrapper validates operands before the C call: a
+    shorter b, a strided view or a CUDA tensor on the host path would make the
+    library multiply (and certify) the wrong digits."""
+    import torch
+    from paper_1006_0405_b200 import _check_operands, _check_out
+    a = torch.zeros((4, 8), dtype=torch.uint8)
+    _check_operands(a, a.clone(), False)
+    with pytest.raises(ValueError):
+        _check_operands(a, torch.zeros((4, 7), dtype=torch.uint8), False)
+    with pytest.raises(ValueError):
+        _check_operands(torch.zeros((4, 16), dtype=torch.uint8)[:, :8], a, False)
+    with pytest.raises(TypeError):
+        _check_operands(a.to(torch.int16), a, False)
+    with pytest.raises(ValueError):
+        _check_operands(a, a, True, 0)  # host tensors on a device entry point
+    with pytest.raises(ValueError):
+        _check_operands(torch.zeros((0, 8), dtype=torch.uint8), torch.zeros((0, 8), dtype=torch.uint8), False)
+    _check_out(torch.zeros((4, 16), dtype=torch.uint8), (4, 16), torch.uint8, False, "out")
+    with pytest.raises(ValueError):
+        _check_out(torch.zeros((4, 15), dtype=torch.uint8), (4, 16), torch.uint8, False, "out")

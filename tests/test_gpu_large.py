@@ -1,10 +1,10 @@
 """GPU parity for the multi-CTA path (m = 2^14 .. 2^18), incl. configs C3 and C5.
 
 Same bars as test_gpu_parity.py.  Full-size configs: every product of C3 is
-checked bit-exact against Python's int multiplication; C5 (65,536 pairs) is
-checked bit-exact on a seeded sample plus the closed form on every all-255
-pair; oracle flags / radii on small samples (the oracle needs seconds per
-pair at these sizes).
+checked bit-exact against Python's int multiplication; every one of C5's 65,536
+products against the exact product modulo two random 61-bit primes,
+the all-255 ones by closed form, a sample by Python ints; oracle flags / radii
+on small samples here (tools/radius_ratios.py records the full distributions).
 """
 import numpy as np
 import pytest
@@ -61,21 +61,69 @@ def test_config_C3_full(ctx):
     print("C3 max radius gpu", g["max_radius"][[0, 32]], "oracle", r["max_radius"])
 
 
-def test_config_C5_sampled(ctx):
-    """C5 shape (16,384 digits, 1/3 uniform, 1/3 all-255, 1/3 sparse) on a
-    4,096-pair slice: all certified; all-255 pairs by closed form; a seeded
-    sample of 48 pairs bit-exact; oracle radius on 3 pairs."""
+def c5_chunks(ctx, chunk=8192):
+    """All 65,536 C5 pairs in chunks, digits generated on the device by the
+    seeded generator (bit-equal to inputs.py, tests/test_inputs.py)."""
     import torch
-    pairs = np.arange(4096)
+    n, B = 16384, 65536
+    kinds_all = inputs.class_of_pairs("C5", B).astype(np.uint8)
+    seed = inputs.config_seed(5)
+    for p0 in range(0, B, chunk):
+        kt = torch.from_numpy(kinds_all[p0:p0 + chunk]).cuda()
+        a = ctx.generate_digits(n, chunk, seed, 0, kind=kt, pair0=p0)
+        b = ctx.generate_digits(n, chunk, seed, 1, kind=kt, pair0=p0)
+        yield p0, a, b, kinds_all[p0:p0 + chunk]
+
+
+def test_config_C5_full(ctx):
+    """C5 (16,384 digits, 1/3 uniform, 1/3 all-255, 1/3 sparse): EVERY one of
+    the 65,536 products is certified and checked -- against the exact product
+    modulo two fresh random 61-bit primes (oracle.residue_check), the
+    all-255 pairs also against the closed form (256^n - 1)^2 -- and 16 pairs per
+    chunk bit-exact against Python ints; the inputs of the first chunk are
+    checked against inputs.py."""
+    import torch
+    primes = oracle.random_primes(2)
+    n = 16384
+    want255 = np.array([1] + [0] * (n - 1) + [254] + [255] * (n - 1), np.uint8)
+    rng = np.random.default_rng(55)
+    checked = 0
+    for p0, a, b, kinds in c5_chunks(ctx):
+        prod, cert = ctx.multiply(a, b)
+        torch.cuda.synchronize()
+        prod, cert = prod.cpu().numpy(), cert.cpu().numpy().astype(bool)
+        ah, bh = a.cpu().numpy(), b.cpu().numpy()
+        if p0 == 0:
+            ra, rb, _ = inputs.config_inputs("C5", pairs=np.arange(64))
+            assert np.array_equal(ah[:64], ra) and np.array_equal(bh[:64], rb)
+        assert cert.all(), np.nonzero(~cert)[0][:8] + p0
+        ok = oracle.residue_check(ah, bh, prod, primes)
+        assert ok.all(), np.nonzero(~ok)[0][:8] + p0
+        assert (prod[kinds == 1] == want255).all()
+        for q in rng.choice(len(ah), 16, replace=False):
+            assert to_int(prod[q]) == to_int(ah[q]) * to_int(bh[q]), p0 + q
+        checked += len(ah)
+    assert checked == 65536
+
+
+def test_config_C5_radius_vs_oracle(ctx):
+    """C5 radius bound (R10) on 6 pairs, two of each kind."""
+    pairs = np.array([0, 1, 2, 3, 4, 5])
     a, b, kinds = inputs.config_inputs("C5", pairs=pairs)
     g = gpu_run(ctx, a, b)
     assert g["cert"].all()
-    n = a.shape[1]
-    want255 = np.array([1] + [0] * (n - 1) + [254] + [255] * (n - 1), np.uint8)
-    for p in np.nonzero(kinds == 1)[0]:
-        assert np.array_equal(g["prod"][p], want255)
-    rng = np.random.default_rng(5)
-    for p in rng.choice(4096, 48, replace=False):
-        assert to_int(g["prod"][p]) == to_int(a[p]) * to_int(b[p]), p
-    r = oracle.ivmul(a[:3], b[:3])
-    assert np.all(g["max_radius"][:3] <= 2 * r["max_radius"]), (g["max_radius"][:3], r["max_radius"])
+    r = oracle.ivmul(a, b)
+    assert np.all(g["max_radius"] <= 2 * r["max_radius"]), (g["max_radius"], r["max_radius"])
+
+
+@pytest.mark.parametrize("n", [5000, 12000, 30000])
+def test_group_kernel_forced_at_cluster_sizes(n, monkeypatch):
+    """IVM_KERNEL=v5: the group kernel at m = 2^14 .. 2^16 (normally the cluster
+    kernel's sizes; the variant the host can pick to fill SMs clusters leave idle)."""
+    import paper_1006_0405_b200 as ivm
+    monkeypatch.setenv("IVM_KERNEL", "v5")
+    c5 = ivm.Context(0)
+    kinds = np.array([0, 1, 2, 3])
+    a, b = inputs.pair_digits(0x55 + n, np.arange(4), n, kinds)
+    check_pairs(c5, a, b, dump_n=2, oracle_sample=[0, 1])
+    c5.close()

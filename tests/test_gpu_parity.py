@@ -43,6 +43,12 @@ def gpu_run(ctx, a, b, prec="f64", dump=None):
     return out
 
 
+def real_interval_kernel(m, prec):
+    """The odd-frequency (R13) kernels compute real coefficient intervals:
+    binary64 m >= 64 (v6, v3, v4, v5), binary32 m >= 1024 (v3, v4, v5)."""
+    return m >= 1024 or (prec == "f64" and m >= 64)
+
+
 def check_pairs(ctx, a, b, prec="f64", dump_n=4, oracle_sample=None, expect_all_cert=True):
     B, n = a.shape
     dump = list(range(min(dump_n, B)))
@@ -64,7 +70,10 @@ def check_pairs(ctx, a, b, prec="f64", dump_n=4, oracle_sample=None, expect_all_
         iv = g["intervals"][j]
         c = exact[p].astype(np.float64)
         assert np.all(iv[:2 * n - 1, 0] <= c) and np.all(c <= iv[:2 * n - 1, 1]), p
-        assert np.all(iv[:, 2] <= 0) and np.all(0 <= iv[:, 3]), p
+        if real_interval_kernel(m, prec):  # imag not computed (R13): NaN
+            assert np.isnan(iv[:, 2:]).all(), p
+        else:
+            assert np.all(iv[:, 2] <= 0) and np.all(0 <= iv[:, 3]), p
         assert np.all(iv[2 * n - 1:, 0] <= 0) and np.all(0 <= iv[2 * n - 1:, 1]), p
         assert iv.shape == (m, 4)
     # (3) oracle flag agreement with margin, radius within 2x
@@ -256,3 +265,32 @@ def test_misaligned_operands_and_products(ctx, n):
     o = out.cpu().numpy()
     for p in range(B):
         assert big(o[p]) == big(a[p]) * big(b[p]), p
+
+
+@pytest.mark.parametrize("n", [4096, 16384])
+def test_two_streams_one_context(ctx, n):
+    """Calls on one context from two streams (include/ivm.h "streams"): the
+    context's scratch is shared, so the second call must wait for the first;
+    both batches must come back exact."""
+    import torch
+    B = 300
+    a1, b1 = inputs.pair_digits(0xA1 + n, np.arange(B), n, "uniform")
+    a2, b2 = inputs.pair_digits(0xA2 + n, np.arange(B), n, "uniform")
+    t = [torch.from_numpy(x).cuda() for x in (a1, b1, a2, b2)]
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    outs = []
+    for rep in range(3):
+        p1, c1 = ctx.multiply(t[0], t[1], stream=s1)
+        p2, c2 = ctx.multiply(t[2], t[3], stream=s2)
+        outs.append((p1, c1, p2, c2))
+    torch.cuda.synchronize()
+    w1 = oracle.long_multiply(a1[:16], b1[:16])
+    w2 = oracle.long_multiply(a2[:16], b2[:16])
+    r1 = oracle.residue_check(a1, b1, outs[0][0].cpu().numpy())
+    r2 = oracle.residue_check(a2, b2, outs[0][2].cpu().numpy())
+    assert r1.all() and r2.all()
+    for p1, c1, p2, c2 in outs:
+        assert c1.cpu().numpy().all() and c2.cpu().numpy().all()
+        assert np.array_equal(p1.cpu().numpy()[:16], w1) and np.array_equal(p2.cpu().numpy()[:16], w2)
+        assert torch.equal(p1, outs[0][0]) and torch.equal(p2, outs[0][2])

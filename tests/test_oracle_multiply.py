@@ -157,3 +157,33 @@ def test_paper_limit_75000_digits_certifies_sample():
     assert r["max_radius"].max() < 0.25
     for p in range(2):
         assert to_int(r["prod"][p]) == to_int(a[p]) * to_int(b[p])
+
+
+def test_residue_check_pins():
+    """S:432 residue check: agrees with Python int arithmetic, accepts every
+    true product and rejects products with one wrong digit."""
+    primes = oracle.random_primes(2, seed=7)
+    for p in primes:
+        assert p.bit_length() == 61 and oracle._is_prime(p)
+    assert oracle._is_prime(2 ** 61 - 1) and not oracle._is_prime((2 ** 61 - 1) * 3)
+    for n in (1, 2, 7, 100, 1000):
+        a, b = inputs.pair_digits(0x7E5 + n, np.arange(8), n, np.array([0, 1, 2, 3, 0, 1, 2, 3]))
+        z = oracle.long_multiply(a, b)
+        assert oracle.residue_check(a, b, z, primes).all()
+        for q in range(8):
+            want = to_int(a[q]) * to_int(b[q])
+            for p in primes:  # the residues the C code compares, by Python ints
+                assert (to_int(a[q]) % p) * (to_int(b[q]) % p) % p == want % p == to_int(z[q]) % p
+        bad = z.copy()
+        rng = np.random.default_rng(n)
+        for q in range(8):
+            i = rng.integers(0, 2 * n)
+            bad[q, i] ^= 1 << int(rng.integers(0, 8))
+        assert not oracle.residue_check(a, b, bad, primes).any()
+    # the paper's limit: a 75,000-digit all-255 pair by its closed form
+    n = 75000
+    a = np.full((1, n), 255, np.uint8)
+    z = np.array([[1] + [0] * (n - 1) + [254] + [255] * (n - 1)], np.uint8)
+    assert oracle.residue_check(a, a, z, primes).all()
+    z[0, n] = 253
+    assert not oracle.residue_check(a, a, z, primes).any()
