@@ -244,6 +244,8 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE {world} ranks were launched")
     if world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
@@ -292,18 +294,45 @@ def run_ours(args):
     ncert = int(cert.sum().item())
     tot_ms = ivd.max_over_ranks(tot_ms, device=dev)
     total_cert = ivd.sum_over_ranks(ncert, device=dev)
-    gather_ms = None
-    if args.gather and world > 1:
+    gather = None
+    if args.gather:
+        # the same step with the products and flags gathered to rank 0, chunk k's
+        # NCCL sends overlapping chunk k+1's multiplication (dist.multiply_gather)
+        # the job: world x the per-rank batch (weak scaling), C5's whole batch (strong)
+        job_batch = batch * world if args.config not in STRONG else CONFIGS[args.config][1]
+        root_p = torch.empty((job_batch, 2 * n), dtype=torch.uint8, device=dev) if rank == 0 else None
+        root_c = torch.empty((job_batch,), dtype=torch.uint8, device=dev) if rank == 0 else None
+
+        def compute(lo, cnt):
+            ctx.multiply(a[lo:lo + cnt], b[lo:lo + cnt], prec=prec, out=out[lo:lo + cnt], cert=cert[lo:lo + cnt])
+
+        for _ in range(max(args.warmup, 1)):
+            ivd.multiply_gather(compute, out, cert, job_batch, chunks=args.gather_chunks, out_prod=root_p,
+                                out_cert=root_c)
         torch.cuda.synchronize()
-        dist.barrier()
-        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        g0.record(s)
-        ivd.gather_to_root(out, cert)
-        g1.record(s)
-        torch.cuda.synchronize()
-        gather_ms = ivd.max_over_ranks(g0.elapsed_time(g1), device=dev)
+        if world > 1:
+            dist.barrier()
+        gms = []
+        for _ in range(args.steps):
+            flush.zero_()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(s)
+            ivd.multiply_gather(compute, out, cert, job_batch, chunks=args.gather_chunks, out_prod=root_p,
+                                out_cert=root_c)
+            g1.record(s)
+            torch.cuda.synchronize()
+            gms.append(g0.elapsed_time(g1))
+        g_ms = ivd.max_over_ranks(sum(gms) / len(gms), device=dev)
+        gcert = int(root_c.sum().item()) if rank == 0 else 0
+        gather = {"ms_per_step": g_ms, "value": gcert * n / (g_ms / 1e3) if rank == 0 else None,
+                  "chunks": args.gather_chunks, "bytes_to_root_per_step": (2 * n + 1) * job_batch,
+                  "method": "per-chunk NCCL isend/irecv to rank 0 overlapped with the next chunk's multiply"}
     ms_per_step = tot_ms / args.steps
     value = total_cert * n / (ms_per_step / 1e3)
+    # one step's summary over the ranks: certified pairs (SUM) and, from a
+    # diagnostic multiply, the max coefficient radius (MAX) -- one collective
+    rad = ctx.multiply_diag(a, b, prec=prec, coeffs=False)["max_radius"]
+    summ_cert, summ_rad = ivd.summary_allreduce(cert, rad)
 
     # ---- end-to-end through the host-pointer C ABI (pinned host buffers) ----
     ha = a.cpu().pin_memory()
@@ -362,7 +391,8 @@ def run_ours(args):
                        "parallelism": f"batch-sharded x{world} (no data-path collective)",
                        "l2": "flushed between timed steps (256 MiB write, outside the events)",
                        "certified_pairs_per_step": total_cert,
-                       "gather_to_rank0_ms": gather_ms},
+                       "summary_allreduce": {"certified_pairs": summ_cert, "max_radius": summ_rad},
+                       "with_gather_to_rank0": gather},
             "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12,
                          "unit": "Top/s (directed FP64 DADD/DMUL/DFMA, FMA = 1 op)",
                          "frac": achieved / peak_ops, "traffic": load_traffic(args.config),
@@ -398,8 +428,14 @@ def main():
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--gather", action="store_true", help="also time the NCCL gather of products to rank 0")
+    ap.add_argument("--gather", action="store_true",
+                    help="also time the step with the products gathered to rank 0 (pipelined NCCL sends)")
+    ap.add_argument("--gather-chunks", type=int, default=4)
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # not started by torchrun: launch the N ranks (one process per GPU) ourselves
+        from paper_1006_0405_b200 import dist as ivd
+        sys.exit(ivd.spawn(args.gpus, os.path.abspath(__file__), sys.argv[1:]))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -196,12 +196,23 @@ int ivm_multi_create(ivm_multi_t *m, int ngpu, const int *devices);
  * cert_shards[g] ([batch_per_gpu]); no data-path collective.  If
  * gather_to_root, the products and flags are gathered in shard order into
  * root_prod ([ngpu * batch_per_gpu][2n]) and root_cert ([ngpu *
- * batch_per_gpu]) on the root device (grouped ncclSend / ncclRecv).  Returns
- * after every device's work (and the gather) completed. */
+ * batch_per_gpu]) on the root device (grouped ncclSend / ncclRecv).  The
+ * gather is pipelined: each shard runs as 4 chunks, and chunk k's sends run on
+ * a communication stream while chunk k+1 multiplies.  Returns after every
+ * device's work (and the gather) completed. */
 int ivm_multi_multiply(ivm_multi_t m, const uint8_t *const *a_shards, const uint8_t *const *b_shards,
                        size_t n, size_t batch_per_gpu, uint8_t *const *prod_shards,
                        uint8_t *const *cert_shards, int prec, int gather_to_root, uint8_t *root_prod,
                        uint8_t *root_cert);
+
+/* The step summary over all devices: *certified_total = the
+ * number of nonzero flags in cert_shards[g][0 .. batch_per_gpu) summed over
+ * the devices, *max_radius = the largest radius_shards[g][i] (device arrays,
+ * e.g. ivm_multiply_batched_diag's max_radius; NaN counts as +inf), or NaN if
+ * radius_shards is NULL (max_radius nullable).  A per-device reduction kernel,
+ * then ncclAllReduce (SUM, MAX) across the devices; synchronous. */
+int ivm_multi_summary(ivm_multi_t m, const uint8_t *const *cert_shards, const double *const *radius_shards,
+                      size_t batch_per_gpu, uint64_t *certified_total, double *max_radius);
 
 /* Destroy the communicators and contexts; NULL is a no-op. */
 int ivm_multi_destroy(ivm_multi_t m);

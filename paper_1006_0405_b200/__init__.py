@@ -24,7 +24,7 @@ EXPORTS = ["ivm_version", "ivm_strerror", "ivm_max_digits", "ivm_fft_length", "i
            "ivm_multiply_batched_diag", "ivm_multiply_batched_host", "ivm_generate_digits",
            "ivm_peak_probe", "ivm_last_launch_count", "ivm_twiddle_table", "ivm_long_multiply_batched",
            "ivm_multiply_exact", "ivm_multiply_naive", "ivm_multiply_disc", "ivm_multi_create",
-           "ivm_multi_multiply", "ivm_multi_destroy"]
+           "ivm_multi_multiply", "ivm_multi_summary", "ivm_multi_destroy"]
 
 
 class IvmError(RuntimeError):
@@ -63,6 +63,7 @@ def lib():
             "ivm_multiply_disc": ([P, P, P, S, S, P, P, P, P], None),
             "ivm_multi_create": ([ctypes.POINTER(P), I, P], None),
             "ivm_multi_multiply": ([P, P, P, S, S, P, P, I, I, P, P], None),
+            "ivm_multi_summary": ([P, P, P, S, P, P], None),
             "ivm_multi_destroy": ([P], None),
         }
         # (an older build missing a symbol fails at that call, not at load:

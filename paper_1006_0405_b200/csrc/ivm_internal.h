@@ -66,6 +66,8 @@ int upload_w64_v5(const double *w64, const float *w32);
 int v5_info(int prec, int m, LaunchInfo *li);
 int v5_launch(int prec, int m, const KParams &kp, const Group5Args &ga, int groups, cudaStream_t s);
 
+// batch summary {certified count, max radius} into out[2] (device), zeroed first
+int summary_launch(const uint8_t *cert, const double *rad, int batch, double *out, cudaStream_t s);
 // circular containment sets, m <= 8192
 int disc_smem(int lg);
 int disc_launch(const uint8_t *a, const uint8_t *b, int n, int batch, int lg, const void *tw, double rw,

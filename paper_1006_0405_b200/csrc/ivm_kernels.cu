@@ -645,4 +645,37 @@ int probe_launch(int prec, int iters, void *sink, int sms, cudaStream_t s, uint6
   return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
 }
 
+// summary of a batch (the multi-GPU all-reduce's local part): out[0] += the
+// number of certified pairs, out[1] = max(out[1], max radius).  out must hold
+// {0, 0} before the launch (radii are >= 0, so a float-bit atomicMax on the
+// unsigned pattern is the max).
+__global__ void ivm_summary_kernel(const uint8_t *cert, const double *rad, int batch, double *out) {
+  unsigned cnt = 0;
+  unsigned long long mx = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < batch; i += gridDim.x * blockDim.x) {
+    cnt += cert[i] != 0;
+    if (rad) {
+      const double r = rad[i];
+      const unsigned long long u = r != r ? 0x7ff0000000000000ull : (unsigned long long)__double_as_longlong(r);
+      mx = u > mx ? u : mx;
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    const unsigned long long v = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = v > mx ? v : mx;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (cnt) atomicAdd(out, (double)cnt);
+    if (mx) atomicMax(reinterpret_cast<unsigned long long *>(out + 1), mx);
+  }
+}
+int summary_launch(const uint8_t *cert, const double *rad, int batch, double *out, cudaStream_t s) {
+  if (cudaMemsetAsync(out, 0, 2 * sizeof(double), s) != cudaSuccess) return -1;
+  int grid = (batch + 255) / 256;
+  grid = grid > 148 ? 148 : grid;
+  ivm_summary_kernel<<<grid, 256, 0, s>>>(cert, rad, batch, out);
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
+}
+
 }  // namespace ivm

@@ -42,6 +42,18 @@ def test_multi_api_matches_single_context():
         assert np.array_equal(rp.cpu().numpy(), oracle.long_multiply(a, b))
         for g in range(ngpu):
             assert np.array_equal(tp[g].cpu().numpy(), rp[g * bpg:(g + 1) * bpg].cpu().numpy())
+        # the summary all-reduce: certified pairs summed, max radius maxed
+        ctxs = [ivm.Context(g) for g in range(ngpu)]
+        rads = [ctxs[g].multiply_diag(ta[g], tb[g], coeffs=False)["max_radius"] for g in range(ngpu)]
+        torch.cuda.synchronize()
+        tot, mr = ctypes.c_uint64(), ctypes.c_double()
+        st = L.ivm_multi_summary(h, arr(tc), arr(rads), bpg, ctypes.byref(tot), ctypes.byref(mr))
+        assert st == 0, st
+        assert tot.value == ngpu * bpg
+        assert mr.value == max(float(r.max().item()) for r in rads) and mr.value > 0
+        tc[0][3] = 0  # one uncertified flag
+        st = L.ivm_multi_summary(h, arr(tc), None, bpg, ctypes.byref(tot), ctypes.byref(mr))
+        assert st == 0 and tot.value == ngpu * bpg - 1 and np.isnan(mr.value)
     finally:
         assert L.ivm_multi_destroy(h) == 0
 
