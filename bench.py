@@ -179,6 +179,7 @@ def cpu_baseline(a, b, n, prec, budget_s=12.0):
     import oracle
     cores = oracle.max_threads()
     B = a.shape[0]
+    oracle.ivmul(a[:1], b[:1], prec=prec)  # builds the twiddle table (mpmath) outside the timing
     k = min(B, max(cores, 1))
     t0 = time.perf_counter()
     r = oracle.ivmul(a[:k], b[:k], prec=prec)
