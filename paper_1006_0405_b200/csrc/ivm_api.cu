@@ -4,6 +4,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <cmath>
 #include <map>
 #include <mutex>
@@ -53,6 +54,11 @@ struct ivm_ctx {
   // the scratch buffers above are shared by every call on the context: a call
   // on another stream than the previous call's waits for the previous call
   cudaEvent_t done_ev = nullptr;
+  // co-run of the group kernel beside the cluster kernel (corun_split)
+  bool corun = true;
+  double corun_eff = 0.75;
+  cudaStream_t s_co = nullptr;
+  cudaEvent_t co_ev[2] = {nullptr, nullptr};
   cudaStream_t last_stream = nullptr;
   bool have_last = false;
 };
@@ -155,7 +161,15 @@ int ivm_create(ivm_ctx_t *ctx, int device) {
   const char *kv = getenv("IVM_KERNEL");
   c->force_v1 = kv && strcmp(kv, "v1") == 0;
   c->force_v5 = kv && strcmp(kv, "v5") == 0;
-  if (cudaEventCreateWithFlags(&c->done_ev, cudaEventDisableTiming) != cudaSuccess) {
+  {  // IVM_CORUN=0 disables the co-run; IVM_CORUN_EFF sets the group kernel's relative rate
+    const char *e = getenv("IVM_CORUN");
+    c->corun = !(e && strcmp(e, "0") == 0);
+    const char *f = getenv("IVM_CORUN_EFF");
+    if (f && atof(f) > 0.05 && atof(f) <= 2.0) c->corun_eff = atof(f);
+  }
+  if (cudaEventCreateWithFlags(&c->done_ev, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->co_ev[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->co_ev[1], cudaEventDisableTiming) != cudaSuccess) {
     delete c;
     return IVM_ECUDA;
   }
@@ -183,6 +197,9 @@ int ivm_destroy(ivm_ctx_t c) {
   if (c->s_out) cudaStreamDestroy(c->s_out);
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   if (c->done_ev) cudaEventDestroy(c->done_ev);
+  for (cudaEvent_t e : c->co_ev)
+    if (e) cudaEventDestroy(e);
+  if (c->s_co) cudaStreamDestroy(c->s_co);
   delete c;
   return IVM_OK;
 }
@@ -336,6 +353,66 @@ static int get_info(ivm_ctx_t c, int m, int prec, ivm::LaunchInfo *li) {
   return IVM_OK;
 }
 
+// exchange / barrier scratch of the group kernel (v5) for `groups` groups of C CTAs
+static int ensure_gscratch5(ivm_ctx_t c, int m, int prec, size_t groups, size_t C) {
+  (void)m;
+  const size_t al = 256, es = prec == IVM_F64 ? 8 : 4;
+  auto up = [&](size_t x) { return (x + al - 1) / al * al; };
+  const size_t need = up(groups * C * 4096 * 4 * es) + up(groups * C * 32) + up(groups * 2 * C * C * 8 * 8) +
+                      up(groups * 2 * C * C) + up(groups * 4);
+  if (c->gscratch_bytes >= need) return IVM_OK;
+  cudaFree(c->gscratch);
+  c->gscratch = nullptr;
+  c->gscratch_bytes = 0;
+  if (cudaMalloc(&c->gscratch, need) != cudaSuccess) return IVM_ENOMEM;
+  c->gscratch_bytes = need;
+  return IVM_OK;
+}
+
+// the group kernel on `groups` groups (scratch ensured by the caller); coop:
+// cooperative launch (the kernel alone on the device), else a plain launch
+// (co-run beside the cluster kernel on the SMs its clusters leave free)
+static int launch_v5(ivm_ctx_t c, int m, int prec, const ivm::KParams &kp0, size_t groups, size_t C, void *ascr,
+                     cudaStream_t s, bool coop) {
+  const size_t al = 256, es = prec == IVM_F64 ? 8 : 4;
+  auto up = [&](size_t x) { return (x + al - 1) / al * al; };
+  const size_t b_x = up(groups * C * 4096 * 4 * es), b_l = up(groups * C * 32),
+               b_b = up(groups * 2 * C * C * 8 * 8), b_bits = up(groups * 2 * C * C), b_ctr = up(groups * 4);
+  char *gs = (char *)c->gscratch;
+  ivm::Group5Args ga;
+  ga.xch = gs;
+  ga.link = (unsigned *)(gs + b_x);
+  ga.bnd = (long long *)(gs + b_x + b_l);
+  ga.bits = (uint8_t *)(gs + b_x + b_l + b_b);
+  ga.ctr = (unsigned *)(gs + b_x + b_l + b_b + b_bits);
+  if (cudaMemsetAsync(ga.ctr, 0, b_ctr, s) != cudaSuccess) return cuda_fail(c);
+  ivm::KParams kp = kp0;
+  kp.ascratch = ascr;
+  if (ivm::v5_launch(prec, m, kp, ga, (int)groups, s, coop) != 0) return cuda_fail(c);
+  return IVM_OK;
+}
+
+// Co-run split of a cluster-kernel batch (m = 2^14 .. 2^16): clusters of C CTAs
+// must sit inside one GPC, so `cl` clusters strand sms - cl C SMs; `g5` groups
+// of the group kernel (same C, exchange through L2) run there at a per-group
+// rate `eff` of a cluster's.  Returns the pairs the group kernel takes so that
+// the two finish together (0: no co-run).
+static size_t corun_split(size_t batch, size_t cl, size_t g5, double eff) {
+  if (g5 == 0 || cl == 0 || batch < 2 * (cl + g5)) return 0;
+  size_t best = 0;
+  double tbest = (double)((batch + cl - 1) / cl);
+  for (size_t r5 = 1; r5 * g5 <= batch; r5++) {
+    const size_t b5 = r5 * g5, b4 = batch - b5;
+    const double t = std::max((double)((b4 + cl - 1) / cl), (double)r5 / eff);
+    if (t < tbest) {
+      tbest = t;
+      best = b5;
+    }
+    if ((double)r5 / eff > tbest) break;
+  }
+  return best;
+}
+
 static int grid_for(ivm_ctx_t c, const ivm::LaunchInfo &li, size_t batch) {
   size_t g = (size_t)c->sms * (size_t)li.blocks_per_sm;
   if (g > batch) g = batch;
@@ -452,13 +529,50 @@ int ivm_multiply_batched_diag(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, s
     r = get_table4(c, m, prec, &tw);
     if (!r) r = get_info4(c, m, prec, &li);
     if (r) return r;
+    const size_t C = (size_t)li.cluster;
     const size_t cl = (size_t)li.max_clusters < batch ? (size_t)li.max_clusters : batch;
-    r = ensure_scratch(c, cl * li.cluster * li.a_bytes_per_cta);
+    // the SMs whole clusters leave free take a share of the batch with the group kernel
+    ivm::LaunchInfo l5;
+    size_t g5 = 0, b5 = 0;
+    if (c->corun && cl == (size_t)li.max_clusters && get_info5(c, m, prec, &l5) == IVM_OK && l5.blocks_per_sm >= 1) {
+      const size_t used = cl * C, free_sms = (size_t)c->sms > used ? (size_t)c->sms - used : 0;
+      g5 = free_sms / C;
+      b5 = corun_split(batch, cl, g5, c->corun_eff);
+    }
+    const size_t b4 = batch - b5;
+    const size_t a4 = cl * C * li.a_bytes_per_cta;
+    r = ensure_scratch(c, a4 + (b5 ? g5 * C * l5.a_bytes_per_cta : 0));
+    if (!r && b5) r = ensure_gscratch5(c, m, prec, g5, C);
+    if (!r && b5 && !c->s_co && cudaStreamCreateWithFlags(&c->s_co, cudaStreamNonBlocking) != cudaSuccess)
+      r = cuda_fail(c);
     if (r) return r;
-    kp.ascratch = c->ascratch;
     kp.tw = tw;
-    if (ivm::v4_launch(prec, m, kp, (int)cl, s) != 0) return cuda_fail(c);
-    c->last_launches = launches + 1;
+    if (b5) {  // the group kernel's stream starts after the work queued on s
+      if (cudaEventRecord(c->co_ev[0], s) != cudaSuccess || cudaStreamWaitEvent(c->s_co, c->co_ev[0], 0) != cudaSuccess)
+        return cuda_fail(c);
+    }
+    kp.batch = (int)b4;
+    kp.ascratch = c->ascratch;
+    if (ivm::v4_launch(prec, m, kp, (int)(cl < b4 ? cl : b4), s) != 0) return cuda_fail(c);
+    launches++;
+    if (b5) {
+      ivm::KParams k5 = kp;
+      k5.batch = (int)b5;
+      k5.a = kp.a + b4 * n;
+      k5.b = kp.b + b4 * n;
+      k5.prod = kp.prod + b4 * 2 * n;
+      k5.cert = kp.cert + b4;
+      if (kp.max_radius) k5.max_radius = kp.max_radius + b4;
+      if (kp.first_bad) k5.first_bad = kp.first_bad + b4;
+      if (kp.coeffs) k5.coeffs = kp.coeffs + b4 * (2 * n - 1);
+      if (kp.dump_slot) k5.dump_slot = kp.dump_slot + b4;
+      r = launch_v5(c, m, prec, k5, g5 < b5 ? g5 : b5, C, (char *)c->ascratch + a4, c->s_co, false);
+      if (r) return r;
+      launches += 1;
+      if (cudaEventRecord(c->co_ev[1], c->s_co) != cudaSuccess || cudaStreamWaitEvent(s, c->co_ev[1], 0) != cudaSuccess)
+        return cuda_fail(c);
+    }
+    c->last_launches = launches;
     return IVM_OK;
   }
   if (use_v6(c, m, prec)) {
@@ -488,30 +602,11 @@ int ivm_multiply_batched_diag(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, s
     if (groups > batch) groups = batch;
     if (groups < 1) return IVM_EUNSUPPORTED;
     r = ensure_scratch(c, groups * C * li.a_bytes_per_cta);
+    if (!r) r = ensure_gscratch5(c, m, prec, groups, C);
     if (r) return r;
-    const size_t al = 256, es = prec == IVM_F64 ? 8 : 4;
-    auto up = [&](size_t x) { return (x + al - 1) / al * al; };
-    const size_t b_x = up(groups * C * 4096 * 4 * es), b_l = up(groups * C * 32),
-                 b_b = up(groups * 2 * C * C * 8 * 8), b_bits = up(groups * 2 * C * C), b_ctr = up(groups * 4);
-    const size_t need = b_x + b_l + b_b + b_bits + b_ctr;
-    if (c->gscratch_bytes < need) {
-      cudaFree(c->gscratch);
-      c->gscratch = nullptr;
-      c->gscratch_bytes = 0;
-      if (cudaMalloc(&c->gscratch, need) != cudaSuccess) return IVM_ENOMEM;
-      c->gscratch_bytes = need;
-    }
-    char *gs = (char *)c->gscratch;
-    ivm::Group5Args ga;
-    ga.xch = gs;
-    ga.link = (unsigned *)(gs + b_x);
-    ga.bnd = (long long *)(gs + b_x + b_l);
-    ga.bits = (uint8_t *)(gs + b_x + b_l + b_b);
-    ga.ctr = (unsigned *)(gs + b_x + b_l + b_b + b_bits);
-    if (cudaMemsetAsync(ga.ctr, 0, b_ctr, s) != cudaSuccess) return cuda_fail(c);
-    kp.ascratch = c->ascratch;
     kp.tw = tw;
-    if (ivm::v5_launch(prec, m, kp, ga, (int)groups, s) != 0) return cuda_fail(c);
+    r = launch_v5(c, m, prec, kp, groups, C, c->ascratch, s, true);
+    if (r) return r;
     c->last_launches = launches + 1;
     return IVM_OK;
   }

@@ -64,7 +64,7 @@ struct Group5Args {
 };
 int upload_w64_v5(const double *w64, const float *w32);
 int v5_info(int prec, int m, LaunchInfo *li);
-int v5_launch(int prec, int m, const KParams &kp, const Group5Args &ga, int groups, cudaStream_t s);
+int v5_launch(int prec, int m, const KParams &kp, const Group5Args &ga, int groups, cudaStream_t s, bool coop);
 
 // batch summary {certified count, max radius} into out[2] (device), zeroed first
 int summary_launch(const uint8_t *cert, const double *rad, int batch, double *out, cudaStream_t s);

@@ -64,7 +64,8 @@ template <int M> static int v5_info_m(int prec, LaunchInfo *li) {
 }
 int v5_info(int prec, int m, LaunchInfo *li) { IVM_V5_DISPATCH(v5_info_m, prec, li) }
 
-template <typename T, int M> static int v5_go(const KParams &kp, const Group5Args &ga, int groups, cudaStream_t s) {
+template <typename T, int M>
+static int v5_go(const KParams &kp, const Group5Args &ga, int groups, cudaStream_t s, bool coop) {
   using CF = v5::Cfg5<T, M>;
   KParams k2 = kp;
   v5::Group5 g{ga.ctr, ga.xch, ga.link, ga.bnd, ga.bits};
@@ -73,16 +74,20 @@ template <typename T, int M> static int v5_go(const KParams &kp, const Group5Arg
   // of zero-padding terms (a separate instantiation: ivm_v4.cuh cross_fwd)
   const bool qb = M == 18 && kp.n <= (1 << (M - 1)) - 8 * 4096;
   const void *fn = qb ? (const void *)v5::ivm_v5_kernel<T, M, M == 18> : (const void *)v5::ivm_v5_kernel<T, M>;
-  return cudaLaunchCooperativeKernel(fn, dim3(groups * v4::G4<M>::C),
-                                     dim3(CF::THREADS), args, CF::SMEM, s) == cudaSuccess
-             ? 0
-             : -1;
+  // coop = false: a plain launch beside the cluster kernel, on the SMs its
+  // clusters leave free (the group barrier needs the group's CTAs co-resident,
+  // which the free SMs give; a CTA placed late only delays its group)
+  const cudaError_t e = coop ? cudaLaunchCooperativeKernel(fn, dim3(groups * v4::G4<M>::C), dim3(CF::THREADS), args,
+                                                         CF::SMEM, s)
+                             : cudaLaunchKernel(fn, dim3(groups * v4::G4<M>::C), dim3(CF::THREADS), args, CF::SMEM, s);
+  return e == cudaSuccess ? 0 : -1;
 }
-template <int M> static int v5_launch_m(int prec, const KParams &kp, const Group5Args &ga, int groups, cudaStream_t s) {
-  return prec == 0 ? v5_go<double, M>(kp, ga, groups, s) : v5_go<float, M>(kp, ga, groups, s);
+template <int M>
+static int v5_launch_m(int prec, const KParams &kp, const Group5Args &ga, int groups, cudaStream_t s, bool coop) {
+  return prec == 0 ? v5_go<double, M>(kp, ga, groups, s, coop) : v5_go<float, M>(kp, ga, groups, s, coop);
 }
-int v5_launch(int prec, int m, const KParams &kp, const Group5Args &ga, int groups, cudaStream_t s) {
-  IVM_V5_DISPATCH(v5_launch_m, prec, kp, ga, groups, s)
+int v5_launch(int prec, int m, const KParams &kp, const Group5Args &ga, int groups, cudaStream_t s, bool coop) {
+  IVM_V5_DISPATCH(v5_launch_m, prec, kp, ga, groups, s, coop)
 }
 
 }  // namespace ivm

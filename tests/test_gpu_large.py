@@ -127,3 +127,39 @@ def test_group_kernel_forced_at_cluster_sizes(n, monkeypatch):
     a, b = inputs.pair_digits(0x55 + n, np.arange(4), n, kinds)
     check_pairs(c5, a, b, dump_n=2, oracle_sample=[0, 1])
     c5.close()
+
+
+@pytest.mark.parametrize("n", [12000, 30000])
+def test_cluster_and_group_corun(n, monkeypatch):
+    """A batch large enough for the co-run (the group kernel on the SMs whole
+    clusters leave free): the same products and flags as the
+    cluster kernel alone (IVM_CORUN=0); certified products exact; diagnostics
+    (radius, first-bad, dumps) land on the right pairs in both portions."""
+    import torch
+    import paper_1006_0405_b200 as ivm
+    B = 400
+    kinds = np.arange(B) % 3
+    a, b = inputs.pair_digits(0xC0 + n, np.arange(B), n, kinds)
+    ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    res = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("IVM_CORUN", mode)
+        cx = ivm.Context(0)
+        r = cx.multiply_diag(ta, tb, dump_pairs=[0, B - 1], coeffs=False)
+        torch.cuda.synchronize()
+        res[mode] = {k: (v.cpu().numpy() if hasattr(v, "cpu") else v) for k, v in r.items()}
+        cx.close()
+    for mode in ("0", "1"):
+        g = res[mode]
+        assert g["cert"].all()
+        assert oracle.residue_check(a, b, g["prod"]).all()
+        assert (g["first_bad"] == -1).all() and (g["max_radius"] > 0).all()
+        exact = oracle.coefficients(a[[0, B - 1]], b[[0, B - 1]])
+        for j in range(2):
+            iv = g["intervals"][j]
+            c = exact[j].astype(np.float64)
+            assert np.all(iv[:2 * n - 1, 0] <= c) and np.all(c <= iv[:2 * n - 1, 1])
+    assert np.array_equal(res["0"]["prod"], res["1"]["prod"])
+    assert np.array_equal(res["0"]["cert"], res["1"]["cert"])
+    o = oracle.ivmul(a[[B - 1]], b[[B - 1]])
+    assert res["1"]["max_radius"][B - 1] <= 2 * o["max_radius"][0]
