@@ -56,7 +56,7 @@ struct ivm_ctx {
   cudaEvent_t done_ev = nullptr;
   // co-run of the group kernel beside the cluster kernel (corun_split)
   bool corun = true;
-  double corun_eff = 0.75;
+  double corun_eff = 0.8;
   cudaStream_t s_co = nullptr;
   cudaEvent_t co_ev[2] = {nullptr, nullptr};
   cudaStream_t last_stream = nullptr;

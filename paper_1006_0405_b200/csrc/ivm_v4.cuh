@@ -20,6 +20,10 @@
 // contiguous word segments with the cluster-level ballot adder.
 #pragma once
 
+#ifndef IVM_QB_GROUP
+#define IVM_QB_GROUP 4
+#endif
+
 namespace ivm {
 namespace v4 {
 
@@ -198,11 +202,12 @@ __device__ __forceinline__ void cross_fwd(const uint8_t *__restrict__ dig, int n
     // unrolled groups of 8.  Otherwise every term, fully unrolled (all loads in
     // flight); one kernel holding both forms measured slower on both paths.
     if constexpr (QB) {
-      const int qmax = (min(C, (n + 4095) >> 12) + 7) & ~7;
+      constexpr int QG = IVM_QB_GROUP;  // terms per unrolled group
+      const int qmax = (min(C, (n + 4095) >> 12) + QG - 1) / QG * QG;
 #pragma unroll 1
-      for (int q0 = 0; q0 < qmax; q0 += 8) {
+      for (int q0 = 0; q0 < qmax; q0 += QG) {
 #pragma unroll
-        for (int qq = 0; qq < 8; qq++) term(q0 + qq);
+        for (int qq = 0; qq < QG; qq++) term(q0 + qq);
       }
     } else {
 #pragma unroll
