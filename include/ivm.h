@@ -178,8 +178,11 @@ int ivm_multiply_naive(ivm_ctx_t ctx, const uint8_t *a, const uint8_t *b, size_t
  * fp64.  a, b: device [batch][n]; prod: device [batch][2n] (zero digits where
  * not certified); cert: device [batch] (1 = proved exact); max_radius:
  * device [batch] largest disc radius over the 2n-1 used coefficients, or NULL.
- * n <= 4096 (m <= 8192; IVM_EUNSUPPORTED otherwise).  Asynchronous on
- * `cuda_stream`; uses context-owned device scratch. */
+ * n <= ivm_max_digits(IVM_F64) (m <= 2^18; IVM_EUNSUPPORTED otherwise): one
+ * CTA per multiplication for m <= 8192, else a group of m/8192 co-resident
+ * CTAs (the same DIT factored as 8192 x m/8192, exchanging through device
+ * scratch).  Asynchronous on `cuda_stream`; uses context-owned device
+ * scratch. */
 int ivm_multiply_disc(ivm_ctx_t ctx, const uint8_t *a, const uint8_t *b, size_t n, size_t batch,
                       uint8_t *prod, uint8_t *cert, double *max_radius, void *cuda_stream);
 

@@ -233,7 +233,7 @@ class Context:
         return out
 
     def multiply_disc(self, a, b, out=None, cert=None, want_radius: bool = True, stream=None):
-        """Circular containment sets (R15), fp64, n <= 4096:
+        """Circular containment sets (R15), fp64, n <= max_digits():
         (products [B][2n] u8, certified [B] u8, max disc radius [B] f64 or None)."""
         import torch
         _check_operands(a, b, True, self.device)

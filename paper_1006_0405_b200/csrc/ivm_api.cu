@@ -898,7 +898,7 @@ int ivm_multiply_naive(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, size_t n
 int ivm_multiply_disc(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, size_t n, size_t batch, uint8_t *prod,
                       uint8_t *cert, double *max_radius, void *stream) {
   if (!c || !a || !b || !prod || !cert || n == 0 || batch == 0) return IVM_EINVAL;
-  if (n > 4096 || batch > (size_t)0x7fffffff) return IVM_EUNSUPPORTED;
+  if (n > ivm_max_digits(IVM_F64) || batch > (size_t)0x7fffffff) return IVM_EUNSUPPORTED;
   if (c->sticky) return c->sticky;
   if (cudaSetDevice(c->device) != cudaSuccess) return cuda_fail(c);
   StreamOrder order(c, stream);
@@ -927,6 +927,27 @@ int ivm_multiply_disc(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, size_t n,
       return cuda_fail(c);
     }
     c->twd[lg] = std::make_pair(w, rw);
+  }
+  if (lg > 13) {  // groups of m/8192 co-resident CTAs (ivm_disc.cu disc_group_kernel)
+    const int nb = ivm::disc_group_blocks_per_sm();
+    if (nb < 1) return cuda_fail(c);
+    const size_t C = (size_t)1 << (lg - 13);
+    size_t groups = (size_t)c->sms * nb / C;
+    if (groups > batch) groups = batch;
+    if (groups < 1) return IVM_EUNSUPPORTED;
+    const size_t need = ivm::disc_group_scratch(lg, groups);
+    if (c->dscratch_bytes < need) {
+      cudaFree(c->dscratch);
+      c->dscratch = nullptr;
+      c->dscratch_bytes = 0;
+      if (cudaMalloc(&c->dscratch, need) != cudaSuccess) return IVM_ENOMEM;
+      c->dscratch_bytes = need;
+    }
+    if (ivm::disc_group_launch(a, b, (int)n, (int)batch, lg, w, rw, c->dscratch, groups, prod, cert, max_radius,
+                               (cudaStream_t)stream) != 0)
+      return cuda_fail(c);
+    c->last_launches = 1;
+    return IVM_OK;
   }
   size_t grid = (size_t)c->sms;
   if (grid > batch) grid = batch;

@@ -68,6 +68,11 @@ int v5_launch(int prec, int m, const KParams &kp, const Group5Args &ga, int grou
 
 // batch summary {certified count, max radius} into out[2] (device), zeroed first
 int summary_launch(const uint8_t *cert, const double *rad, int batch, double *out, cudaStream_t s);
+// circular containment sets, m = 2^14 .. 2^18: groups of m/8192 CTAs
+int disc_group_blocks_per_sm();
+size_t disc_group_scratch(int lg, size_t groups);
+int disc_group_launch(const uint8_t *a, const uint8_t *b, int n, int batch, int lg, const void *tw, double rw,
+                      void *scratch, size_t groups, uint8_t *prod, uint8_t *cert, double *max_radius, cudaStream_t s);
 // circular containment sets, m <= 8192
 int disc_smem(int lg);
 int disc_launch(const uint8_t *a, const uint8_t *b, int n, int batch, int lg, const void *tw, double rw,

@@ -442,6 +442,22 @@ __device__ __forceinline__ void certify_real(T lo, T hi, int i, int n, D *dst, C
   }
 }
 
+// experiment build only (-DIVM_DUMP_PREROT, tools/untwist_cost.py): the dump's
+// otherwise-NaN imaginary slots of coefficients k and k + m/2 carry the real and
+// imaginary part of the packed value before the final untwist rotation (scaled
+// by 2/m), so the rotation's share of the coefficient widths can be measured
+template <typename T>
+__device__ __forceinline__ void dump_prerot(double *dump, int k, int N, const CI<T> &o, T s) {
+#ifdef IVM_DUMP_PREROT
+  if (dump) {
+    reinterpret_cast<double2 *>(dump)[2 * k + 1] =
+        make_double2((double)DR<T>::mul_rd(o.rl, s), (double)DR<T>::mul_ru(o.rh, s));
+    reinterpret_cast<double2 *>(dump)[2 * (k + N / 2) + 1] =
+        make_double2((double)DR<T>::mul_rd(o.il, s), (double)DR<T>::mul_ru(o.ih, s));
+  }
+#endif
+}
+
 __device__ __forceinline__ void cert_flush(const CertAcc &acc, Cert3 &cs) {
   const int ok = __reduce_and_sync(0xffffffffu, (unsigned)acc.ok);
   const int bad = (int)__reduce_min_sync(0xffffffffu, (unsigned)acc.bad);
@@ -470,6 +486,7 @@ __device__ __forceinline__ void emit_coeffs(const CI<T> &o, int k, const TwC<T> 
   const T s = T(2) / T(N);  // exact power of two
   certify_real(DR<T>::mul_rd(v.rl, s), DR<T>::mul_ru(v.rh, s), k, n, coef + k, acc, dump);
   certify_real(DR<T>::mul_rd(v.il, s), DR<T>::mul_ru(v.ih, s), k + N / 2, n, coef + k + N / 2, acc, dump);
+  dump_prerot(dump, k, N, o, s);
 }
 
 // folded variant: the input twiddles already carried z^{-k0}; the remaining
@@ -483,6 +500,7 @@ __device__ __forceinline__ void emit_fold(const CI<T> &o, int r, int k, int n, i
   const T s = T(2) / T(N);
   certify_real(DR<T>::mul_rd(v.rl, s), DR<T>::mul_ru(v.rh, s), k, n, d0, acc, dump);
   certify_real(DR<T>::mul_rd(v.il, s), DR<T>::mul_ru(v.ih, s), k + N / 2, n, d1, acc, dump);
+  dump_prerot(dump, k, N, o, s);
 }
 
 template <typename T, int M, int RK, bool WARP = false>

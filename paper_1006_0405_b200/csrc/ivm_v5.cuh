@@ -122,6 +122,7 @@ __device__ __forceinline__ void emit_tab(const CI<T> &o, const TwC<T> &w, int k,
   const T s = T(2) / T(N);
   certify_real(DR<T>::mul_rd(v.rl, s), DR<T>::mul_ru(v.rh, s), k, n, d0, acc, dump);
   certify_real(DR<T>::mul_rd(v.il, s), DR<T>::mul_ru(v.ih, s), k + N / 2, n, d1, acc, dump);
+  dump_prerot(dump, k, N, o, s);
 }
 
 // QB: the cross pass skips its zero-padding terms in groups of 8 (host picks it

@@ -70,6 +70,54 @@ def test_disc_batch_ragged_and_deterministic(ctx):
 def test_disc_rejects_too_large(ctx):
     import torch
     import paper_1006_0405_b200 as ivm
-    t = torch.zeros((1, 4097), dtype=torch.uint8, device="cuda")
+    t = torch.zeros((1, ivm.max_digits() + 1), dtype=torch.uint8, device="cuda")
     with pytest.raises(ivm.IvmError):
         ctx.multiply_disc(t, t)
+
+
+@pytest.mark.parametrize("n", [4097, 5000, 8193, 12000, 20000, 40000])
+def test_disc_group_parity_with_oracle(ctx, n):
+    """m = 2^14 .. 2^17: the group kernel (8192 x m/8192 DIT factorization)
+    against the disc oracle: products bit-exact, flags where the oracle
+    certifies with margin, radius within 2x (and not below 1/4)."""
+    K = inputs.KINDS
+    kinds = np.array([K["uniform"], K["all255"], K["sparse"], K["msd"]])
+    a, b = inputs.pair_digits(0xD15E + n, np.arange(4), n, kinds)
+    prod, cert, rad = run(ctx, a, b)
+    ref = oracle.disc_mul(a, b)
+    assert ref["cert"].all() and cert.all()
+    assert np.array_equal(prod, oracle.long_multiply(a, b))
+    floor = 1e-30
+    ratio = np.maximum(rad, floor) / np.maximum(ref["max_radius"], floor)
+    assert (ratio <= 2.0).all() and (ratio >= 0.25).all(), (n, ratio)
+
+
+def test_disc_group_C3_size(ctx):
+    """The paper's limit (C3 shape, n = 75,000, m = 2^18, 32 CTAs per
+    multiplication): a uniform and an all-255 pair certified and exact, the
+    radius within 2x of the disc oracle's, and (P:290's question) far below the
+    rectangular oracle's."""
+    n = 75000
+    a, b = inputs.pair_digits(inputs.config_seed(3), np.arange(2), n, np.array([0, 1]))
+    a[1] = 255
+    b[1] = 255
+    prod, cert, rad = run(ctx, a, b)
+    assert cert.all()
+    to_int = lambda d: int.from_bytes(bytes(d), "little")
+    for p in range(2):
+        assert to_int(prod[p]) == to_int(a[p]) * to_int(b[p])
+    ref = oracle.disc_mul(a, b)
+    assert (rad <= 2 * ref["max_radius"]).all() and (rad >= 0.25 * ref["max_radius"]).all()
+    rect = oracle.ivmul(a, b)
+    assert (rad < rect["max_radius"]).all(), (rad, rect["max_radius"])
+
+
+def test_disc_group_batch_deterministic(ctx):
+    """More pairs than groups (persistent loop), two runs bitwise identical."""
+    n = 9000
+    B = 40
+    a, b = inputs.pair_digits(0xD160, np.arange(B), n, np.arange(B) % 3)
+    p1, c1, r1 = run(ctx, a, b)
+    p2, c2, r2 = run(ctx, a, b)
+    assert np.array_equal(p1, p2) and np.array_equal(c1, c2) and np.array_equal(r1, r2)
+    assert c1.all() and oracle.residue_check(a, b, p1).all()
