@@ -105,3 +105,19 @@ def test_binding_operand_checks():
     _check_out(torch.zeros((4, 16), dtype=torch.uint8), (4, 16), torch.uint8, False, "out")
     with pytest.raises(ValueError):
         _check_out(torch.zeros((4, 15), dtype=torch.uint8), (4, 16), torch.uint8, False, "out")
+
+
+@pytest.mark.parametrize("prec", [ivm.F64, ivm.F32])
+@pytest.mark.parametrize("log2m", [16, 17, 18, 19])
+def test_planner_twiddles_large_m_sampled(log2m, prec):
+    """The tables the large-m kernels plan (up to 2^(m+1) = 2^19 for C3):
+    sampled entries, every octant and the quarter-turn points, equal to the
+    oracle's direct mpmath enclosure of omega_N^j (no symmetry used)."""
+    N = 1 << log2m
+    lib_tw = ivm.twiddle_table(log2m, prec)
+    p = "f64" if prec == ivm.F64 else "f32"
+    rng = np.random.default_rng(log2m)
+    js = set(rng.integers(0, N, 48).tolist()) | {0, 1, N // 8, N // 8 + 1, N // 4 - 1, N // 4, N // 2 + 3, N - 1}
+    for j in sorted(js):
+        want = np.array(oracle.direct_enclosure(N, j, p), dtype=lib_tw.dtype)
+        assert np.array_equal(lib_tw[j], want), (N, j, lib_tw[j], want)

@@ -1,10 +1,10 @@
 """Circular vs rectangular containment sets (R15), measured.
 
 GPU part (needs a B200): device throughput of ivm_multiply_disc and of the
-rectangular path (ivm_multiply_batched) on the same seeded inputs, CUDA events,
-L2 flushed between reps; and the largest radius of each over uniform and
-all-255 pairs.  CPU part (--oracle): the two oracles' radii at sizes the disc
-kernel does not cover (n up to 131072).
+rectangular path (ivm_multiply_batched) on the same seeded inputs (up to the
+C3 workload), CUDA events, L2 flushed between reps; and the largest radius of
+each over uniform and all-255 pairs, n = 32 .. 131072.  CPU part (--oracle):
+the two oracles' radii (n up to 131072).
 
     python tools/disc_bench.py [--out gpurun_out/disc.json]
     python tools/disc_bench.py --oracle [--out profiles/r01/disc_oracle_radii.json]
@@ -42,9 +42,14 @@ def gpu(args):
             ts.append(e0.elapsed_time(e1))
         return sorted(ts)[len(ts) // 2]
 
-    for n, B in ((1000, 4096), (4096, 4096)):
-        a = ctx.generate_digits(n, B, 1, 0)
-        b = ctx.generate_digits(n, B, 1, 1)
+    for n, B in ((1000, 4096), (4096, 4096), (16384, 2048), (75000, 64)):
+        if n == 75000:  # config C3: half uniform, half all-255
+            kinds = torch.from_numpy(inputs.class_of_pairs("C3", B).astype(np.uint8)).cuda()
+            a = ctx.generate_digits(n, B, inputs.config_seed(3), 0, kind=kinds)
+            b = ctx.generate_digits(n, B, inputs.config_seed(3), 1, kind=kinds)
+        else:
+            a = ctx.generate_digits(n, B, 1, 0)
+            b = ctx.generate_digits(n, B, 1, 1)
         t_d = timed(lambda: ctx.multiply_disc(a, b, want_radius=False))
         t_r = timed(lambda: ctx.multiply(a, b))
         _, cd, _ = ctx.multiply_disc(a, b, want_radius=False)
@@ -54,9 +59,9 @@ def gpu(args):
             "disc_digits_per_s": n * B / (t_d / 1e3), "rect_digits_per_s": n * B / (t_r / 1e3),
             "disc_certified": float(cd.float().mean()), "rect_certified": float(cr.float().mean())})
         print(res["throughput"][-1], flush=True)
-    for n in (32, 256, 1000, 4096):
+    for n in (32, 256, 1000, 4096, 16384, 75000, 131072):
         for kind in ("uniform", "all255"):
-            a, b = inputs.pair_digits(0xD15E + n, np.arange(64), n, kind)
+            a, b = inputs.pair_digits(0xD15E + n, np.arange(64 if n <= 16384 else 8), n, kind)
             ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
             _, cd, rd = ctx.multiply_disc(ta, tb)
             rr = ctx.multiply_diag(ta, tb)
