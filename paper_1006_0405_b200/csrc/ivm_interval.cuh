@@ -29,8 +29,9 @@ template <> struct DR<double> {
   static __device__ __forceinline__ double mul_ru(double a, double b) { return __dmul_ru(a, b); }
   static __device__ __forceinline__ double fma_rd(double a, double b, double c) { return __fma_rd(a, b, c); }
   static __device__ __forceinline__ double fma_ru(double a, double b, double c) { return __fma_ru(a, b, c); }
-  // sign bit set (x < 0 or x == -0.0)
-  static __device__ __forceinline__ bool neg(double x) { return __double_as_longlong(x) < 0; }
+  // sign bit set (x < 0 or x == -0.0): a test of the high word only (a 64-bit
+  // compare costs two ISETPs)
+  static __device__ __forceinline__ bool neg(double x) { return __double2hiint(x) < 0; }
 };
 template <> struct DR<float> {
   static __device__ __forceinline__ float add_rd(float a, float b) { return __fadd_rd(a, b); }

@@ -187,6 +187,21 @@ __device__ __forceinline__ CI<T> q1mul(T c, T s, const CI<T> &d) {
   return t;
 }
 
+// w * conj(d) for a compact first-quadrant w = c + i s, without materialising
+// conj(d): q1mul's formulas with d.il -> -d.ih, d.ih -> -d.il (the sign bits
+// flip, the negations become free FMA operand modifiers)
+template <typename T>
+__device__ __forceinline__ CI<T> q1mul_cd(T c, T s, const CI<T> &d) {
+  using B = TB<T>;
+  const unsigned nxl = B::sgn(d.rl), nxh = B::sgn(d.rh), nyl = B::sgn(d.il), nyh = B::sgn(d.ih);
+  CI<T> t;
+  t.rl = DR<T>::fma_rd(B::sel(s, nyl), d.il, DR<T>::mul_rd(B::sel(c, nxl), d.rl));
+  t.rh = DR<T>::fma_ru(B::sel(s, 1u - nyh), d.ih, DR<T>::mul_ru(B::sel(c, 1u - nxh), d.rh));
+  t.il = DR<T>::fma_rd(B::sel(s, nxl), d.rl, DR<T>::mul_rd(B::sel(c, 1u - nyh), -d.ih));
+  t.ih = DR<T>::fma_ru(B::sel(s, 1u - nxh), d.rh, DR<T>::mul_ru(B::sel(c, nyl), -d.il));
+  return t;
+}
+
 // w = c (1 + i) (c == s, i.e. w_8): the c- and s-selects coincide (4 instead of 8)
 template <typename T>
 __device__ __forceinline__ CI<T> q1mul_eq(T c, const CI<T> &d) {
@@ -198,6 +213,20 @@ __device__ __forceinline__ CI<T> q1mul_eq(T c, const CI<T> &d) {
   t.rh = DR<T>::fma_ru(-cyl, d.il, DR<T>::mul_ru(cxh, d.rh));
   t.il = DR<T>::fma_rd(cxl, d.rl, DR<T>::mul_rd(cyl, d.il));
   t.ih = DR<T>::fma_ru(cxh, d.rh, DR<T>::mul_ru(cyh, d.ih));
+  return t;
+}
+
+// conj(d) variant of q1mul_eq (see q1mul_cd)
+template <typename T>
+__device__ __forceinline__ CI<T> q1mul_eq_cd(T c, const CI<T> &d) {
+  using B = TB<T>;
+  const unsigned nxl = B::sgn(d.rl), nxh = B::sgn(d.rh), nyl = B::sgn(d.il), nyh = B::sgn(d.ih);
+  const T cxl = B::sel(c, nxl), cxh = B::sel(c, 1u - nxh), cya = B::sel(c, nyl), cyb = B::sel(c, 1u - nyh);
+  CI<T> t;
+  t.rl = DR<T>::fma_rd(cya, d.il, DR<T>::mul_rd(cxl, d.rl));
+  t.rh = DR<T>::fma_ru(cyb, d.ih, DR<T>::mul_ru(cxh, d.rh));
+  t.il = DR<T>::fma_rd(cxl, d.rl, DR<T>::mul_rd(cyb, -d.ih));
+  t.ih = DR<T>::fma_ru(cxh, d.rh, DR<T>::mul_ru(cya, -d.il));
   return t;
 }
 
@@ -215,15 +244,27 @@ template <typename T, bool CONJ, bool MAYROT = true>
 __device__ __forceinline__ CI<T> rtmul(const TwC<T> &w, const CI<T> &d) {
   using B = TB<T>;
   if constexpr (!MAYROT) {  // the table guarantees k = 0 (angle < pi/2) and s >= 0
-    CI<T> t = q1mul(w.c, w.s, CONJ ? cconj(d) : d);
+    CI<T> t = CONJ ? q1mul_cd(w.c, w.s, d) : q1mul(w.c, w.s, d);
     return CONJ ? cconj(t) : t;
   } else {
     const unsigned k = B::sgn(w.s);
     const T s = B::absb(w.s);
-    CI<T> t = q1mul(w.c, s, CONJ ? cconj(d) : d);
+    CI<T> t = CONJ ? q1mul_cd(w.c, s, d) : q1mul(w.c, s, d);
     t = rot_if(t, k);
     return CONJ ? cconj(t) : t;
   }
+}
+
+// (CONJ ? conj(w) : w) * conj(d) for a runtime table twiddle (a mirrored input
+// read without materialising its conjugate): conj(w) conj(d) = conj(w d)
+template <typename T, bool CONJ, bool MAYROT = true>
+__device__ __forceinline__ CI<T> rtmul_cd(const TwC<T> &w, const CI<T> &d) {
+  using B = TB<T>;
+  const unsigned k = MAYROT ? B::sgn(w.s) : 0u;
+  const T s = MAYROT ? B::absb(w.s) : w.s;
+  CI<T> t = CONJ ? q1mul(w.c, s, d) : q1mul_cd(w.c, s, d);
+  if constexpr (MAYROT) t = rot_if(t, k);
+  return CONJ ? cconj(t) : t;
 }
 
 template <typename T>
@@ -256,14 +297,14 @@ __device__ __forceinline__ CI<T> ctw(const CI<T> &o, int j, int M) {
   if (4 * j < M) {  // first quadrant
     const int e = j * (64 / M);
     const TwC<T> w = cw64<T>(e);
-    if (e == 8) return INV ? cconj(q1mul_eq(w.c, cconj(o))) : q1mul_eq(w.c, o);  // w_8
-    return INV ? cconj(q1mul(w.c, w.s, cconj(o))) : q1mul(w.c, w.s, o);
+    if (e == 8) return INV ? cconj(q1mul_eq_cd(w.c, o)) : q1mul_eq(w.c, o);  // w_8
+    return INV ? cconj(q1mul_cd(w.c, w.s, o)) : q1mul(w.c, w.s, o);
   }
   // second quadrant: w = i * w', w' = w_M^{j - M/4}
   const int e = (j - M / 4) * (64 / M);
   const TwC<T> w = cw64<T>(e);
-  if (e == 8) return INV ? mul_mi(cconj(q1mul_eq(w.c, cconj(o)))) : mul_i(q1mul_eq(w.c, o));
-  return INV ? mul_mi(cconj(q1mul(w.c, w.s, cconj(o)))) : mul_i(q1mul(w.c, w.s, o));
+  if (e == 8) return INV ? mul_mi(cconj(q1mul_eq_cd(w.c, o))) : mul_i(q1mul_eq(w.c, o));
+  return INV ? mul_mi(cconj(q1mul_cd(w.c, w.s, o))) : mul_i(q1mul(w.c, w.s, o));
 }
 
 __host__ __device__ constexpr int brev3(int i, int bits) {  // non-recursive: folds after unrolling
@@ -310,6 +351,13 @@ template <typename T> struct Buf {
   __device__ __forceinline__ void st(int i, const CI<T> &z) const {
     re[i] = typename V2t<T>::t{z.rl, z.rh};
     im[i] = typename V2t<T>::t{z.il, z.ih};
+  }
+  // stores conj(z): the imaginary endpoints negated and swapped by flipping
+  // sign bits in the integer pipe (the compiler would otherwise negate with
+  // FP64 DADDs, ~6 % of the FP64 instructions of the one-CTA kernel)
+  __device__ __forceinline__ void st_conj(int i, const CI<T> &z) const {
+    re[i] = typename V2t<T>::t{z.rl, z.rh};
+    im[i] = typename V2t<T>::t{TB<T>::neg(z.ih), TB<T>::neg(z.il)};
   }
 };
 
@@ -359,7 +407,7 @@ __device__ __forceinline__ void fwd_first(const uint8_t *__restrict__ dig, int n
 #pragma unroll
       for (int r = 0; r < R; r++) {
         if (r < R / 2) st.st(sidx(L * r, nu, RSo, SWo), v[g][r]);
-        else st.st(sidx(L * R - 1 - L * r, nu, RSo, SWo), cconj(v[g][r]));
+        else st.st_conj(sidx(L * R - 1 - L * r, nu, RSo, SWo), v[g][r]);
       }
     }
   }
@@ -386,11 +434,11 @@ __device__ __forceinline__ void inv_load_compute(Buf<T> st, const TwC<T> *__rest
 #pragma unroll
     for (int q = 0; q < Q; q++) {
       CI<T> z;
-      if (2 * q < Q) z = st.ld(sidx(k0, nu + Sp * q, RSi, SWi));
-      else z = cconj(st.ld(sidx(k0, S - 1 - nu - Sp * q, RSi, SWi)));
-      if (q > 0) {
-        const TwC<T> w = ldg_twc(tw, TW + (q - 1) * L + k0);
-        z = (2 * q < Q) ? rtmul<T, true>(w, z) : rtmul<T, false>(w, z);
+      if (2 * q < Q) {
+        z = st.ld(sidx(k0, nu + Sp * q, RSi, SWi));
+        if (q > 0) z = rtmul<T, true>(ldg_twc(tw, TW + (q - 1) * L + k0), z);
+      } else {  // the mirror's conjugate, times the twiddle (q >= Q/2 > 0)
+        z = rtmul_cd<T, false>(ldg_twc(tw, TW + (q - 1) * L + k0), st.ld(sidx(k0, S - 1 - nu - Sp * q, RSi, SWi)));
       }
       v[g][q] = z;
     }
@@ -617,15 +665,19 @@ __device__ __forceinline__ void invR(Buf<T> st, const TwC<T> *twb, const PassRT 
 #pragma unroll
   for (int q = 0; q < R; q++) {
     CI<T> z;
-    if (2 * q < R) z = st.ld(base + ((nu + Sp * q) ^ sw));
-    else z = cconj(st.ld(base + ((S - 1 - nu - Sp * q) ^ sw)));
-    if (q > 0 || FOLD) {
+    // unfolded: angle of w_{LQ}^{q' k0} < q' 2pi / Q (q' = min(q, Q-q) <= Q/2): no
+    // rotation unless q' > Q/4
+    const int qq = (2 * q < R) ? q : R - q;
+    if (2 * q < R) {
+      z = st.ld(base + ((nu + Sp * q) ^ sw));
+      if (q > 0 || FOLD) {
+        const TwC<T> w = tp[q * pp.L];
+        z = (FOLD || 4 * qq > R) ? rtmul<T, true, true>(w, z) : rtmul<T, true, false>(w, z);
+      }
+    } else {  // the mirror's conjugate times the twiddle, the conjugate never materialised
+      const CI<T> d = st.ld(base + ((S - 1 - nu - Sp * q) ^ sw));
       const TwC<T> w = tp[q * pp.L];
-      // unfolded: angle of w_{LQ}^{q' k0} < q' 2pi / Q (q' = min(q, Q-q) <= Q/2): no
-      // rotation unless q' > Q/4
-      const int qq = (2 * q < R) ? q : R - q;
-      if (2 * q < R) z = (FOLD || 4 * qq > R) ? rtmul<T, true, true>(w, z) : rtmul<T, true, false>(w, z);
-      else z = (FOLD || 4 * qq > R) ? rtmul<T, false, true>(w, z) : rtmul<T, false, false>(w, z);
+      z = (FOLD || 4 * qq > R) ? rtmul_cd<T, false, true>(w, d) : rtmul_cd<T, false, false>(w, d);
     }
     v[q] = z;
   }
@@ -778,7 +830,7 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
 #pragma unroll
           for (int r = 0; r < R; r++) {
             if (2 * r < R) st.st(sidx(k0 + pp.L * r, nu, pp.RSo, pp.SWo), v[r]);
-            else st.st(sidx(R * pp.L - 1 - k0 - pp.L * r, nu, pp.RSo, pp.SWo), cconj(v[r]));
+            else st.st_conj(sidx(R * pp.L - 1 - k0 - pp.L * r, nu, pp.RSo, pp.SWo), v[r]);
           }
         } else if (op == 0) {  // last pass of a: spectrum class k0 -> A
 #pragma unroll

@@ -217,7 +217,10 @@ __device__ __forceinline__ void cross_fwd(const uint8_t *__restrict__ dig, int n
 #pragma unroll
     for (int h = 0; h < 2; h++)
 #pragma unroll
-      for (int e = 0; e < 4; e++) st.st(4 * t + e + 2048 * h, odd ? cconj(acc[4 * h + e]) : acc[4 * h + e]);
+      for (int e = 0; e < 4; e++) {
+        if (odd) st.st_conj(4 * t + e + 2048 * h, acc[4 * h + e]);
+        else st.st(4 * t + e + 2048 * h, acc[4 * h + e]);
+      }
     return;
   }
 #pragma unroll
@@ -231,7 +234,10 @@ __device__ __forceinline__ void cross_fwd(const uint8_t *__restrict__ dig, int n
   }
   if (wait_cluster) cluster_wait();  // the previous pair's remote reads of this state are done
 #pragma unroll
-  for (int j = 0; j < 8; j++) st.st(t + 512 * j, odd ? cconj(acc[j]) : acc[j]);
+  for (int j = 0; j < 8; j++) {
+    if (odd) st.st_conj(t + 512 * j, acc[j]);
+    else st.st(t + 512 * j, acc[j]);
+  }
 }
 
 template <typename T, int M> struct Cfg4 {
@@ -347,7 +353,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
 #pragma unroll
           for (int r = 0; r < R; r++) {
             if (2 * r < R) st.st(sidx(k0 + pp.L * r, nu, pp.RSo, pp.SWo), v[r]);
-            else st.st(sidx(R * pp.L - 1 - k0 - pp.L * r, nu, pp.RSo, pp.SWo), cconj(v[r]));
+            else st.st_conj(sidx(R * pp.L - 1 - k0 - pp.L * r, nu, pp.RSo, pp.SWo), v[r]);
           }
         } else if (op == 0) {
 #pragma unroll
@@ -403,7 +409,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
           const V r = dsm_ld(dsm_map_addr(re0 + (unsigned)(sizeof(V) * k0), src), (V *)nullptr);
           const V m = dsm_ld(dsm_map_addr(im0 + (unsigned)(sizeof(V) * k0), src), (V *)nullptr);
           const CI<T> z{r.x, r.y, m.x, m.y};
-          v[g][q] = (2 * q < C) ? z : cconj(z);
+          v[g][q] = z;  // the mirrors (2 q >= C) are conjugated by the twiddle product below
         }
       }
       // (no cluster barrier here: the coefficients do not overwrite the state)
@@ -414,7 +420,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
 #pragma unroll
         for (int q = 0; q < C; q++) {
           const TwC<T> w = twb[X::S_SWAP + q * B + kl];
-          v[g][q] = (2 * q < C) ? rtmul<T, true, true>(w, v[g][q]) : rtmul<T, false, true>(w, v[g][q]);
+          v[g][q] = (2 * q < C) ? rtmul<T, true, true>(w, v[g][q]) : rtmul_cd<T, false, true>(w, v[g][q]);
         }
         cdft<T, C, true>(v[g]);
       }

@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
 #pragma unroll
           for (int r = 0; r < R; r++) {
             if (2 * r < R) st.st(sidx(k0 + pp.L * r, nu, pp.RSo, pp.SWo), v[r]);
-            else st.st(sidx(R * pp.L - 1 - k0 - pp.L * r, nu, pp.RSo, pp.SWo), cconj(v[r]));
+            else st.st_conj(sidx(R * pp.L - 1 - k0 - pp.L * r, nu, pp.RSo, pp.SWo), v[r]);
           }
         } else if (op == 0) {
 #pragma unroll
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
           const int src = (2 * q < C) ? 2 * q : 2 * C - 1 - 2 * q;
           const CI<T> z = ldcg_ci(xch + (size_t)src * 4096 + (int)crank * B + kl);
           const TwC<T> w = twb[X::S_SWAP + q * B + kl];
-          v[g][q] = (2 * q < C) ? rtmul<T, true, true>(w, z) : rtmul<T, false, true>(w, cconj(z));
+          v[g][q] = (2 * q < C) ? rtmul<T, true, true>(w, z) : rtmul_cd<T, false, true>(w, z);
         }
         cdft<T, C, true>(v[g]);
       }
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
         const int src = (2 * q < C) ? 2 * q : 2 * C - 1 - 2 * q;
         CI<T> z = ldcg_ci(xch + (size_t)src * 4096 + (int)crank * B + kl);
         const TwC<T> w = twb[X::S_SWAP + q * B + kl];
-        z = (2 * q < C) ? rtmul<T, true, true>(w, z) : rtmul<T, false, true>(w, cconj(z));
+        z = (2 * q < C) ? rtmul<T, true, true>(w, z) : rtmul_cd<T, false, true>(w, z);
         st.st(idx, z);
       }
       __syncthreads();

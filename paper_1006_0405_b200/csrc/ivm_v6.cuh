@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v6_kernel(KParams kp) {
 #pragma unroll
           for (int r = 0; r < R; r++) {
             if (2 * r < R) st.st(sidx(k0 + pp.L * r, nu, pp.RSo, pp.SWo), v[r]);
-            else st.st(sidx(R * pp.L - 1 - k0 - pp.L * r, nu, pp.RSo, pp.SWo), cconj(v[r]));
+            else st.st_conj(sidx(R * pp.L - 1 - k0 - pp.L * r, nu, pp.RSo, pp.SWo), v[r]);
           }
         } else if (op == 0) {
 #pragma unroll
