@@ -233,6 +233,52 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def time_config(ctx, cfg, steps, flush, dev):
+    """Device time of one other config on this rank (N = 1 runs): the same
+    protocol as the main measurement (inputs resident, L2 flushed outside the
+    events, warm-up first); returns its summary for the line's other_configs."""
+    import numpy as np
+    import torch
+    import paper_1006_0405_b200 as ivm
+    from paper_1006_0405_b200 import inputs
+    n, batch, prec_s, kind, _ = CONFIGS[cfg]
+    seed = inputs.config_seed(int(cfg[1:]))
+    if isinstance(kind, str):
+        kind = torch.from_numpy(inputs.class_of_pairs(kind, batch).astype(np.uint8)).to(dev)
+    a = ctx.generate_digits(n, batch, seed, 0, kind=kind)
+    b = ctx.generate_digits(n, batch, seed, 1, kind=kind)
+    out = torch.empty((batch, 2 * n), dtype=torch.uint8, device=dev)
+    cert = torch.empty((batch,), dtype=torch.uint8, device=dev)
+    for _ in range(3):
+        ctx.multiply(a, b, out=out, cert=cert)
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    ms = []
+    sampler = ClockSampler(dev.index if dev.index is not None else 0)
+    sampler.start()
+    for _ in range(steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        ctx.multiply(a, b, out=out, cert=cert)
+        e1.record(s)
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    clocks = sampler.stop()
+    t = sum(ms) / len(ms)
+    ncert = int(cert.sum().item())
+    m = ivm.fft_length(n)
+    peaks = load_peaks()
+    peak_ops = 148 * 64 * peaks.get("sm_max_mhz", 1965.0) * 1e6
+    r = {"workload": CONFIGS[cfg][4], "ms_per_step": t, "steps": steps, "value": ncert * n / (t / 1e3),
+         "unit": UNIT, "certified_pairs": ncert, "batch": batch,
+         "roofline_frac": W_ops(m) * batch / (t / 1e3) / peak_ops, "gpu_launches_per_step": ctx.last_launch_count,
+         "clocks": clocks}
+    del a, b, out, cert
+    torch.cuda.empty_cache()
+    return r
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -335,6 +381,13 @@ def run_ours(args):
     rad = ctx.multiply_diag(a, b, prec=prec, coeffs=False)["max_radius"]
     summ_cert, summ_rad = ivd.summary_allreduce(cert, rad)
 
+    # ---- the other configs, same protocol, so the driver's run records them too ----
+    others = None
+    if world == 1 and args.other_configs:
+        others = {}
+        for cfg in [c for c in args.other_configs.split(",") if c and c != args.config]:
+            others[cfg] = time_config(ctx, cfg, max(3, min(args.steps, 10)), flush, dev)
+
     # ---- end-to-end through the host-pointer C ABI (pinned host buffers) ----
     ha = a.cpu().pin_memory()
     hb = b.cpu().pin_memory()
@@ -415,6 +468,7 @@ def run_ours(args):
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
             "cpu_baseline": cb,
+            "other_configs": others,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -432,6 +486,8 @@ def main():
     ap.add_argument("--gather", action="store_true",
                     help="also time the step with the products gathered to rank 0 (pipelined NCCL sends)")
     ap.add_argument("--gather-chunks", type=int, default=4)
+    ap.add_argument("--other-configs", default="C1,C3,C5",
+                    help="at N = 1 also time these configs (same protocol) into the line's other_configs; '' for none")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # not started by torchrun: launch the N ranks (one process per GPU) ourselves
