@@ -101,6 +101,24 @@ extern "C" {
 
 const char *ivm_version(void) { return "ivm 0.1.0 sm_100a"; }
 
+#ifdef IVM_PHASES
+// experiment build only (tools/phases.py): per-CTA cycle counts of the kernel
+// phases (ivm_phase.cuh); slots [0, 1024) the main kernel, [1024, 2048) the co-run
+static unsigned long long *g_phases = nullptr;
+static constexpr size_t PH_SLOTS = 2048 * 16;
+static unsigned long long *phases_buf() {
+  if (!g_phases && cudaMalloc(&g_phases, PH_SLOTS * 8) == cudaSuccess) cudaMemset(g_phases, 0, PH_SLOTS * 8);
+  return g_phases;
+}
+extern "C" int ivm_phases_read(unsigned long long *out, size_t count) {
+  if (!g_phases || count > PH_SLOTS) return IVM_EINVAL;
+  if (cudaDeviceSynchronize() != cudaSuccess || cudaMemcpy(out, g_phases, count * 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
+      cudaMemset(g_phases, 0, PH_SLOTS * 8) != cudaSuccess)
+    return IVM_ECUDA;
+  return IVM_OK;
+}
+#endif
+
 const char *ivm_strerror(int s) {
   switch (s) {
     case IVM_OK: return "ok";
@@ -504,6 +522,9 @@ int ivm_multiply_batched_diag(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, s
   kp.n = (int)n; kp.batch = (int)batch;
   kp.max_radius = max_radius; kp.first_bad = first_bad; kp.coeffs = coeffs;
   kp.intervals = intervals;
+#ifdef IVM_PHASES
+  kp.phases = phases_buf();
+#endif
   int launches = 0;
   if (n_dump) {
     if (c->slot_cap < batch) {
@@ -566,6 +587,7 @@ int ivm_multiply_batched_diag(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, s
       if (kp.first_bad) k5.first_bad = kp.first_bad + b4;
       if (kp.coeffs) k5.coeffs = kp.coeffs + b4 * (2 * n - 1);
       if (kp.dump_slot) k5.dump_slot = kp.dump_slot + b4;
+      if (kp.phases) k5.phases = kp.phases + 1024 * 16;
       r = launch_v5(c, m, prec, k5, g5 < b5 ? g5 : b5, C, (char *)c->ascratch + a4, c->s_co, false);
       if (r) return r;
       launches += 1;

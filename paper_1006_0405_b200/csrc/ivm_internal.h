@@ -17,6 +17,7 @@ struct KParams {
   int64_t *coeffs;           // [batch][2n-1] nullable
   const int32_t *dump_slot;  // [batch] slot or -1 (nullable)
   double *intervals;         // [n_dump][m][4]
+  unsigned long long *phases;  // [grid][16] SM cycles per phase (-DIVM_PHASES experiment builds only)
 };
 
 struct LaunchInfo {

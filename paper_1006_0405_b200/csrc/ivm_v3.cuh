@@ -15,6 +15,7 @@
 // threads holds a whole half-spectrum in registers while a pass runs in place.
 // Index rules are prototyped in tools/proto_v3.py.
 #pragma once
+#include "ivm_phase.cuh"
 
 namespace ivm {
 namespace v3 {
@@ -794,6 +795,7 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
   // forward-last wait parity 0 (trivially complete in the first pair).  dbar:
   // one phase per pair.
   if (blockIdx.x < kp.batch) mbar_wait(&tbar, 0);
+  IVM_PH_DECL
   for (int pair = blockIdx.x; pair < kp.batch; pair += gridDim.x) {
     const int nxt = pair + (int)gridDim.x;
     if (!staged && nxt < kp.batch) {  // L2 prefetch of the next pair's digits
@@ -818,6 +820,7 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
         bulk_copy(sdig, kp.a + (size_t)nxt * n, n, &dbar);
         bulk_copy(sdig + n, kp.b + (size_t)nxt * n, n, &dbar);
       }
+      IVM_PH(2 * op);
 #pragma unroll 1
       for (int i = 0; i < NFWD; i++) {
         const PassRT pp = pick_fwd<M, R>(i);
@@ -855,6 +858,7 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
         }
         __syncthreads();
       }
+      IVM_PH(2 * op + 1);
     }
     CertAcc acc;
     acc.radius = kp.max_radius != nullptr;
@@ -882,8 +886,10 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
       __syncthreads();
     }
     if constexpr (!LAST16) inv_last<T, M, R>(st, tw, n, coef, acc, diag_dump(kp, pair, N));
+    IVM_PH(4);
     cert_flush(acc, cs);
     __syncthreads();
+    IVM_PH(5);
     if (LAST16 && threadIdx.x == 0 && nxt < kp.batch) {  // restore the forward-last table
       mbar_expect(&tbar, FL_BYTES);
       bulk_copy(twb, tw + Gm::tw_fwd(Gm::P.nf - 1), FL_BYTES, &tbar);
@@ -900,6 +906,7 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
       if (kp.first_bad) kp.first_bad[pair] = certified ? -1 : cs.first_bad;
     }
     __syncthreads();
+    IVM_PH(6);
   }
 }
 

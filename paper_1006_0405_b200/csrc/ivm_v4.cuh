@@ -307,6 +307,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
   // 3 it + 2 (last inverse pass) -> parities it&1, (it+1)&1, it&1
 
   int it = 0;
+  IVM_PH_DECL
   for (int pair = cid; pair < kp.batch; pair += ncl, it++) {
     const unsigned par = (unsigned)it & 1u;
     if (!staged && pair + ncl < kp.batch) {  // L2 prefetch of the next pair's digits (this CTA's slice)
@@ -334,6 +335,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
         cs.maxrad = 0ull;
       }
       __syncthreads();
+      IVM_PH(2 * op);
       if (staged && threadIdx.x == 0) {  // the next operand: b of this pair, or a of the next
         const uint8_t *nx = op == 0 ? kp.b + (size_t)pair * n : kp.a + (size_t)(pair + ncl) * n;
         if (op == 0 || pair + ncl < kp.batch) {
@@ -377,6 +379,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
         }
         __syncthreads();
       }
+      IVM_PH(2 * op + 1);
     }
     CertAcc acc;
 #pragma unroll 1
@@ -395,7 +398,9 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
       mbar_expect(&tbar, EB * 4096);
       bulk_copy(twb + X::S_SWAP, tw + X::XINV(crank), EB * 4096, &tbar);
     }
+    IVM_PH(4);
     cluster_sync();  // (1) every CTA's column of the 4096 rows is in its shared memory
+    IVM_PH(5);
     {
       constexpr int G = 8 / C;  // rows (tasks) per thread
       CI<T> v[G][C];
@@ -437,7 +442,9 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
     }
     cert_flush(acc, cs);
     __syncthreads();
+    IVM_PH(6);
     cluster_sync();  // (3) coefficients and per-CTA certificates complete
+    IVM_PH(7);
     // the C per-CTA certificates: lane p of warp 0 reads CTA p's, the warp
     // reduces, shared memory broadcasts (one remote read per CTA, not per thread)
     __shared__ int s_ok, s_bad;
@@ -464,6 +471,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
       }
     }
     __syncthreads();
+    IVM_PH(8);
     const int ok = s_ok, bad = s_bad;
     const unsigned long long rad = s_rad;
     // carry: coefficient chunk ch (B coefficients, B/4 words) lives in CTA ch mod C
@@ -483,7 +491,9 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
       s_chunk[lc][0] = gen;
       s_chunk[lc][1] = allp;
     }
+    IVM_PH(9);
     cluster_sync();  // (4) every chunk's generate / all-propagate published
+    IVM_PH(10);
     if (ok) {
       if (threadIdx.x < 32) {  // carries into all chunks: the ballot adder over 2C^2 bits
         unsigned G[4], P[4];
@@ -527,6 +537,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
     // overwrites them: arrive now, wait just before the next state write (and
     // the next forward-last table, which replaces the coefficients)
     cluster_arrive_release();
+    IVM_PH(11);
   }
   if (it > 0) cluster_wait();  // no CTA leaves while its shared memory may still be read
 }

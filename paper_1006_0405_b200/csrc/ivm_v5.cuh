@@ -171,6 +171,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
   if (gi < kp.batch) mbar_wait(&tbar, 0);
 
   int it = 0;
+  IVM_PH_DECL
   for (int pair = gi; pair < kp.batch; pair += ngr, it++) {
     const unsigned par = (unsigned)it & 1u;
     if (pair + ngr < kp.batch) {  // L2 prefetch of the next pair's digits (this CTA's slice)
@@ -190,6 +191,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
         cs.maxrad = 0ull;
       }
       __syncthreads();
+      IVM_PH(2 * op);
 #pragma unroll 1
       for (int i = 0; i < 4; i++) {
         const PassRT pp = pick_fwd4<M>(i);
@@ -226,6 +228,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
         }
         __syncthreads();
       }
+      IVM_PH(2 * op + 1);
     }
 #pragma unroll 1
     for (int i = 0; i < 3; i++) {
@@ -245,12 +248,14 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
       }
     }
     __syncthreads();
+    IVM_PH(4);
     if (threadIdx.x == 0) {  // last inverse pass table (this role's rows)
       mbar_expect(&tbar, EB * 4096);
       bulk_copy(twb + X::S_SWAP, tw + X::XINV(crank), EB * 4096, &tbar);
     }
     gsync(ctr, C, gen);  // (1) all columns written
     mbar_wait(&tbar, par);
+    IVM_PH(5);
     CertAcc acc;
     // the coefficients (int64): fp64 two-stage into the twiddle swap buffer (free
     // until the next pair's forward-last table, fetched after the carry), else
@@ -355,6 +360,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
     }
     cert_flush(acc, cs);
     __syncthreads();
+    IVM_PH(6);
     // chunk ch (global, B coefficients from ch B) is local chunk lc = ch / C of CTA ch % C
     // teams: one warp per chunk and NCH / 16 rounds (C >= 8), else one round of
     // 16 / NCH warps per chunk
@@ -373,6 +379,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
       link[crank * 8 + 3] = (unsigned)(cs.maxrad >> 32);
     }
     gsync(ctr, C, gen);  // (2) certificates and chunk boundaries of every CTA visible
+    IVM_PH(7);
     // the group's certificate: warp 0 reads the C link records (L2) and broadcasts;
     // meanwhile the other warps fetch the boundary coefficients before each own chunk
     __shared__ int s_ok, s_bad;
@@ -408,6 +415,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
       }
     }
     __syncthreads();
+    IVM_PH(8);
     const int ok = s_ok, bad = s_bad;
     const unsigned long long rad = s_rad;
     const int words = (nout + 3) / 4, warp = (int)threadIdx.x >> 5;
@@ -422,7 +430,9 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
       if (ok) carry_seg_scan(src, nc, kb, ke, seg, gn, ap, w0, TWP);
       if ((int)threadIdx.x == 32 * w0) bits[ch] = (uint8_t)(gn | (ap << 1));
     }
+    IVM_PH(9);
     gsync(ctr, C, gen);  // (3) every chunk's generate / all-propagate visible
+    IVM_PH(10);
     if (ok) {
       if (threadIdx.x < 32) {  // carries into all 2C^2 chunks: 64 chunks per lane, then across lanes
         const int l = (int)threadIdx.x;
@@ -489,6 +499,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
       }
     }
     __syncthreads();  // coefficients read before the next pair's state / table writes
+    IVM_PH(11);
     if (threadIdx.x == 0 && pair + ngr < kp.batch) {  // next pair's forward-last table
       mbar_expect(&tbar, EB * X::FLAST);
       bulk_copy(twb + X::S_SWAP, tw + X::FWD(crank) + X::FP(4), EB * X::FLAST, &tbar);
