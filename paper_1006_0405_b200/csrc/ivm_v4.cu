@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string.h>
+#include <math.h>
 
 #include "ivm_interval.cuh"
 #include "ivm_internal.h"
@@ -82,6 +83,38 @@ template <typename F, int M> static int v4_tables_impl(const F *w2N /* [2m][4] *
   for (int j = 0; j < C; j++) {  // compact upper-half roots: w_C^j (2j <= C) or w_C^{C-j}; z^{4096 j}
     put(X::S2 + 2 * j, (long)(2 * j <= C ? j : C - j) * (N2 / C));
     put(X::FO + 2 * j, (long)j * 4096);
+  }
+  // the tensor-core cross pass (fp64, C >= 16, ivm_v5.cuh cross_tc): theta_q = T_q 2^-54 + err,
+  // |err| <= 3 2^-55, T_q = round(mid(theta_q) 2^54) as 7 balanced base-256 digits d_i
+  // (T = sum_i d_i 256^i).  B operand s (s < 4) of role c: int8 [8 columns n][32 q] at byte
+  // 1024 c + 256 s; column n = 2 u + e holds part (u & 1) (re / im), digit 2 s + e, except
+  // (s, e) = (3, 1): ones (sum_q x_q, the error's multiplier)
+  if (sizeof(F) == 8 && C >= 16) {
+    int8_t *lb = reinterpret_cast<int8_t *>(out + 2L * X::LIMB);
+    for (int c = 0; c < C; c++)
+      for (int q = 0; q < C; q++)
+        for (int p = 0; p < 2; p++) {
+          const F *th = out + 2L * (X::TH(c) + 2 * q);  // (re.lo, re.hi, im.lo, im.hi)
+          const long double lo = th[2 * p], hi = th[2 * p + 1];
+          const long double sc = 18014398509481984.0L;  // 2^54
+          const long long T = llroundl((lo + hi) / 2 * sc);
+          const long double e = 3.0L / 36028797018963968.0L;  // 3 2^-55
+          const long double tv = (long double)T / sc;
+          if (!(lo <= hi) || fabsl(lo - tv) > e || fabsl(hi - tv) > e) return -4;
+          int8_t d[8];
+          long long r = T;
+          for (int i = 0; i < 7; i++) {
+            long long di = ((r % 256) + 256) % 256;  // balanced digit in [-128, 127]
+            if (di >= 128) di -= 256;
+            d[i] = (int8_t)di;
+            r = (r - di) / 256;
+          }
+          if (r != 0) return -4;
+          d[7] = 1;
+          for (int s = 0; s < 4; s++)
+            for (int u = p; u < 4; u += 2)
+              for (int e2 = 0; e2 < 2; e2++) lb[1024 * c + 256 * s + 32 * (2 * u + e2) + q] = d[2 * s + e2];
+        }
   }
   return ok ? X::TOTAL : -4;
 }

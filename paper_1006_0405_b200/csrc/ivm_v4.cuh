@@ -53,7 +53,11 @@ template <int M> struct G4 {
   __host__ __device__ static constexpr int TH(int c) { return INV + 4096 + C * 4096 + 2 * C * c; }
   static constexpr int S2 = INV + 4096 + C * 4096 + 2 * C * C;
   static constexpr int FO = S2 + 2 * C;
-  static constexpr int TOTAL = FO + 2 * C;
+  //   LIMB:   v5's tensor-core cross pass (fp64, C >= 16): role c at byte offset 1024 c,
+  //           int8 [4 operands s][8 columns][32 q] (see cross_tc in ivm_v5.cuh); 64 C
+  //           entries of 16 B (filled for fp64 only)
+  static constexpr int LIMB = FO + 2 * C;
+  static constexpr int TOTAL = LIMB + 64 * C;
   // shared-memory twiddle area (entries)
   static constexpr int S_SWAP = 0;          // 4096: forward-last -> inverse pass 3 -> last inverse pass
   static constexpr int S_MF = 4096;         // forward passes 1..3 (511 entries + 1 pad)

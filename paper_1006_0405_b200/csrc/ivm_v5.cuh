@@ -82,6 +82,141 @@ struct ChunkSrc {
   __device__ __forceinline__ unsigned long long one(int i) const { return get(i); }
 };
 
+// ---------------------------------------------------------------------------
+// Tensor-core cross pass (fp64, C = 16, 32).  Row c of the first radix-C pass,
+//   G[c][v] = sum_{q<C} theta_q x[v + 4096 q]   (theta_q: this role's twiddles),
+// is a dense contraction of exact small integers once theta_q is written as
+// T_q 2^-54 + err_q with T_q an integer (|err_q| <= 3 2^-55, checked by the
+// table builder): the digits (u8) times T_q's seven balanced base-256 digits
+// (s8) are summed EXACTLY by int8 MMAs (int32 accumulators: |sum| < 2^20),
+// 16 columns x 8 limb rows x 32 q per mma.m16n8k32; the limb sums are
+// recombined exactly in int64 and the only rounding is the final one:
+//   G in [RD(S 2^-54 - E), RU(S 2^-54 + E)],  S = sum_q x_q T_q,  E = 3 2^-55 sum_q x_q
+// (sum_q x_q is an eighth limb row of ones).  Exactness makes the interval
+// tighter than the FP64 direct sum's and no directed rounding is needed until
+// the end.  A fragment (digits, 16 columns x 32 q, row-major): lane (g, t) holds
+// column rows g and g+8 for q = 4t..4t+3 and 16+4t..16+4t+3, built from 32-bit
+// word loads (4 consecutive columns of one q) by 4x4 byte transposes; B
+// fragments (four operands s per role, loaded once per call): column n = 2u + e
+// holds limb 2s + e of part u & 1, so lane (g, t) of operand s receives limbs
+// 2s, 2s+1 of part t & 1 for column rows g, g+8 (C fragment) and after the four
+// MMAs holds all limbs of its part: lane t finishes (part t & 1, row t >> 1) with
+// no cross-lane traffic (the four lanes of a group share the A fragment).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void mma_u8s8(int (&d)[4], unsigned a0, unsigned a1, unsigned a2, unsigned a3,
+                                         unsigned b0, unsigned b1) {
+  asm(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%10,%10,%10,%10};"
+      : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "r"(0));
+}
+
+// o_j = (w0[j], w1[j], w2[j], w3[j]) (bytes, low first)
+__device__ __forceinline__ void tr4x4(unsigned w0, unsigned w1, unsigned w2, unsigned w3, unsigned (&o)[4]) {
+  const unsigned t0 = __byte_perm(w0, w1, 0x5140), t1 = __byte_perm(w0, w1, 0x7362);
+  const unsigned t2 = __byte_perm(w2, w3, 0x5140), t3 = __byte_perm(w2, w3, 0x7362);
+  o[0] = __byte_perm(t0, t2, 0x5410);
+  o[1] = __byte_perm(t0, t2, 0x7632);
+  o[2] = __byte_perm(t1, t3, 0x5410);
+  o[3] = __byte_perm(t1, t3, 0x7632);
+}
+
+// this lane's B fragments (role crank): operand s -> {bf[2 s], bf[2 s + 1]} (k = 4t.., 16+4t..; n = g)
+__device__ __forceinline__ void tc_limbs(const void *tab, unsigned crank, unsigned (&bf)[8]) {
+  const unsigned *lt = reinterpret_cast<const unsigned *>(reinterpret_cast<const uint8_t *>(tab) + 1024u * crank);
+  const unsigned lane = threadIdx.x & 31u, g = lane >> 2, t = lane & 3u;
+#pragma unroll
+  for (int s = 0; s < 4; s++) {
+    bf[2 * s] = __ldg(lt + 64u * s + g * 8u + t);
+    bf[2 * s + 1] = __ldg(lt + 64u * s + g * 8u + 4u + t);
+  }
+}
+
+// 4 consecutive digits (columns v .. v+3 of one q row) as a word, zero past n
+// (rem = n - index of p: the word is wholly inside or outside when WORDS)
+template <bool WORDS>
+__device__ __forceinline__ unsigned tc_ld4(const uint8_t *__restrict__ p, int rem) {
+  if constexpr (WORDS) {
+    return rem > 0 ? __ldg(reinterpret_cast<const unsigned *>(p)) : 0u;
+  } else {
+    unsigned w = 0u;
+#pragma unroll
+    for (int e = 0; e < 4; e++)
+      if (e < rem) w |= (unsigned)__ldg(p + e) << (8 * e);
+    return w;
+  }
+}
+
+// the 16 words of one 64-column group (columns vb ..): [fragment register r][q offset i];
+// every address is the lane's base plus a compile-time offset
+template <int C, bool WORDS>
+__device__ __forceinline__ void tc_load_group(const uint8_t *__restrict__ dig, int n, int vb, int g, int t,
+                                              unsigned (&wv)[4][4]) {
+  const int b0 = vb + 4 * g + 4096 * 4 * t;  // column vb + 4g, q = 4t
+  const uint8_t *p = dig + b0;
+  const int rem = n - b0;
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    wv[0][i] = tc_ld4<WORDS>(p + 4096 * i, rem - 4096 * i);
+    wv[1][i] = tc_ld4<WORDS>(p + 32 + 4096 * i, rem - 32 - 4096 * i);
+    wv[2][i] = C > 16 ? tc_ld4<WORDS>(p + 65536 + 4096 * i, rem - 65536 - 4096 * i) : 0u;
+    wv[3][i] = C > 16 ? tc_ld4<WORDS>(p + 65536 + 32 + 4096 * i, rem - 65536 - 32 - 4096 * i) : 0u;
+  }
+}
+
+template <int M, bool WORDS>
+__device__ __forceinline__ void cross_tc_impl(const uint8_t *__restrict__ dig, int n, Buf<double> st,
+                                              const unsigned (&bf)[8], bool odd) {
+  constexpr int C = G4<M>::C;
+  static_assert(C == 16 || C == 32, "K = 32 (C = 16: the upper half of K is zero)");
+  const int lane = (int)(threadIdx.x & 31u), warp = (int)(threadIdx.x >> 5), g = lane >> 2, t = lane & 3;
+  const bool rowhi = t >= 2, im = (t & 1) != 0;  // this lane finishes (part t & 1, column row t >> 1)
+  unsigned nx[4][4];  // the next group's words, loaded while this group computes
+  tc_load_group<C, WORDS>(dig, n, warp * 256, g, t, nx);
+#pragma unroll 1
+  for (int grp = 0; grp < 4; grp++) {  // 64 columns per group, 4 groups per warp (16 warps x 256)
+    const int vb = warp * 256 + grp * 64;
+    unsigned a[4][4];  // [fragment register][tile j]
+#pragma unroll
+    for (int r = 0; r < 4; r++) tr4x4(nx[r][0], nx[r][1], nx[r][2], nx[r][3], a[r]);
+    if (grp < 3) tc_load_group<C, WORDS>(dig, n, vb + 64, g, t, nx);
+#pragma unroll
+    for (int j = 0; j < 4; j++) {  // tile j: column rows g -> vb + 4g + j, g+8 -> vb + 32 + 4g + j
+      // operand s gives lane t the limb sums D_2s, D_2s+1 of its part (s = 3: D_6, sum x)
+      int x[4][2];
+#pragma unroll
+      for (int s = 0; s < 4; s++) {
+        int d[4];
+        mma_u8s8(d, a[0][j], a[1][j], a[2][j], a[3][j], bf[2 * s], bf[2 * s + 1]);
+        x[s][0] = rowhi ? d[2] : d[0];
+        x[s][1] = rowhi ? d[3] : d[1];
+      }
+      // S = sum_i D_i 256^i = Lo + 2^32 H (exact: |Lo|, |H| < 2^45)
+      const long long Lo = (long long)(x[0][0] + 256 * x[0][1]) + 65536ll * (long long)(x[1][0] + 256 * x[1][1]);
+      const long long H = (long long)(x[2][0] + 256 * x[2][1]) + 65536ll * (long long)x[3][0];
+      const double E = (double)x[3][1] * 8.326672684688674e-17;  // 3 2^-55 sum_q x_q (exact)
+      const double Hd = (double)H, Ld = (double)Lo;
+      const double lo = __fma_rd(Hd, 2.384185791015625e-07, __fma_rd(Ld, 5.551115123125783e-17, -E));
+      const double hi = __fma_ru(Hd, 2.384185791015625e-07, __fma_ru(Ld, 5.551115123125783e-17, E));
+      // one store per lane into its part's plane (the conjugate of odd roles by sign flips)
+      const int v = vb + (rowhi ? 32 : 0) + 4 * g + j;
+      const bool cj = im && odd;
+      const double l2 = cj ? TB<double>::neg(hi) : lo, h2 = cj ? TB<double>::neg(lo) : hi;
+      (im ? st.im : st.re)[v] = make_double2(l2, h2);
+    }
+  }
+}
+
+template <int M>
+__device__ __forceinline__ void cross_tc(const uint8_t *__restrict__ dig, int n, Buf<double> st, const void *limbs,
+                                         unsigned crank) {
+  unsigned bf[8];  // (reloaded per call: L1-resident, and no registers held across the passes)
+  tc_limbs(limbs, crank, bf);
+  if (((reinterpret_cast<uintptr_t>(dig) | (uintptr_t)n) & 3) == 0) cross_tc_impl<M, true>(dig, n, st, bf, (crank & 1u) != 0u);
+  else cross_tc_impl<M, false>(dig, n, st, bf, (crank & 1u) != 0u);
+}
+
 // group barrier: the CTA's writes (ordered before thread 0 by the block barrier)
 // are released by thread 0's gpu-scope release add; the poll acquires the other
 // CTAs' releases
@@ -170,6 +305,12 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
   }
   if (gi < kp.batch) mbar_wait(&tbar, 0);
 
+  // fp64, C >= 16: the cross pass on the tensor cores (exact int8 MMAs, cross_tc)
+#ifdef IVM_NO_TC
+  constexpr bool TCX = false;
+#else
+  constexpr bool TCX = sizeof(T) == 8 && C >= 16;
+#endif
   int it = 0;
   IVM_PH_DECL
   for (int pair = gi; pair < kp.batch; pair += ngr, it++) {
@@ -184,7 +325,8 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
     }
 #pragma unroll 1
     for (int op = 0; op < 2; op++) {
-      cross_fwd<T, M, QB>((op == 0 ? kp.a : kp.b) + (size_t)pair * n, n, st, theta, crank, false, true);
+      if constexpr (TCX) cross_tc<M>((op == 0 ? kp.a : kp.b) + (size_t)pair * n, n, st, tw + X::LIMB, crank);
+      else cross_fwd<T, M, QB>((op == 0 ? kp.a : kp.b) + (size_t)pair * n, n, st, theta, crank, false, true);
       if (op == 1 && threadIdx.x == 0) {
         cs.ok = 1;
         cs.first_bad = 0x7fffffff;
