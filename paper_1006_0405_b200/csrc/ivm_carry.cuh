@@ -199,3 +199,98 @@ static __device__ __forceinline__ void carry_store(const int32_t *coef, int n, u
 }
 
 }  // namespace ivm
+
+namespace ivm {
+
+// Coefficient i of the one-CTA kernel lives at cpos<QS>(i): quad Q (c_4Q .. c_4Q+3)
+// at quad slot (Q & 3) QS + Q / 4, so that thread t's quads 4t .. 4t+3 (its four
+// words) are QS slots apart and a warp's 16-byte reads of them hit consecutive
+// slots (no bank conflicts).  QS = 0: linear.
+template <int QS>
+__device__ __forceinline__ int cpos(int i) {
+  if constexpr (QS == 0) {
+    return i;
+  } else {
+    const int Q = i >> 2;
+    return ((((Q & 3) * QS) + (Q >> 2)) << 2) | (i & 3);
+  }
+}
+
+// One-pass carry with four consecutive words per thread (words 4t .. 4t+3, word
+// k = c_4k .. c_4k+3, P:229-235 in the word form above): every thread forms its
+// u_k, generate and propagate bits in registers (two more words below its own
+// come from the quads 4t-2, 4t-1), one ballot adder over the warp's lanes and
+// one over the block's warps give each thread its carry-in, and its 16 digit
+// bytes are stored at once.  coef: cpos<QS> layout in shared memory, QS =
+// blockDim.x (>= the number of words / 4); out: [2n] digits (global).
+template <int QS>
+static __device__ __forceinline__ void carry_store4(const int32_t *coef, int n, uint8_t *__restrict__ out,
+                                                    bool certified) {
+  const int nout = 2 * n, nc = 2 * n - 1, words = (nout + 3) / 4;
+  const int t = (int)threadIdx.x, lane = t & 31, warp = t >> 5, nwarps = (int)(blockDim.x >> 5);
+  if (!certified) {
+    for (int i = t; i < nout; i += blockDim.x) out[i] = 0;
+    return;
+  }
+  __shared__ unsigned s_wgp[32];
+  unsigned lo[6], hi[6];
+#pragma unroll
+  for (int j = 0; j < 6; j++) {  // words 4t-2 .. 4t+3
+    const int Q = 4 * t - 2 + j;
+    unsigned long long v = 0ull;
+    if (Q >= 0 && 4 * Q < nc) {
+      const int4 q = *reinterpret_cast<const int4 *>(coef + cpos<QS>(4 * Q));
+      const unsigned long long c1 = 4 * Q + 1 < nc ? (unsigned)q.y : 0u, c2 = 4 * Q + 2 < nc ? (unsigned)q.z : 0u,
+                               c3 = 4 * Q + 3 < nc ? (unsigned)q.w : 0u;
+      v = (unsigned long long)(unsigned)q.x + (c1 << 8) + (c2 << 16) + (c3 << 24);
+    }
+    lo[j] = (unsigned)v;
+    hi[j] = (unsigned)(v >> 32);
+  }
+  // W_k = lo_k + hi_{k-1} = w_k + e_k 2^32;  u_k = w_k + e_{k-1} <= 2^32
+  unsigned w[6], e[6];
+#pragma unroll
+  for (int j = 1; j < 6; j++) {
+    w[j] = lo[j] + hi[j - 1];
+    e[j] = w[j] < lo[j] ? 1u : 0u;
+  }
+  unsigned u[4];
+  bool g[4], p[4];
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    u[i] = w[i + 2] + e[i + 1];
+    g[i] = e[i + 1] != 0u && w[i + 2] == 0xffffffffu;
+    p[i] = u[i] == 0xffffffffu && !g[i];
+  }
+  const bool G = g[3] || (p[3] && (g[2] || (p[2] && (g[1] || (p[1] && g[0])))));
+  const bool P = p[0] && p[1] && p[2] && p[3];
+  const unsigned Gw = __ballot_sync(0xffffffffu, G), Pw = __ballot_sync(0xffffffffu, P);
+  if (lane == 0) {
+    const unsigned gen = (unsigned)((((unsigned long long)(Gw | Pw)) + Gw) >> 32);
+    s_wgp[warp] = gen | ((Pw == 0xffffffffu ? 1u : 0u) << 1);
+  }
+  __syncthreads();
+  const unsigned wb = lane < nwarps ? s_wgp[lane] : 0u;
+  const unsigned G2 = __ballot_sync(0xffffffffu, (wb & 1u) != 0u), P2 = __ballot_sync(0xffffffffu, (wb & 2u) != 0u);
+  const unsigned cw = ((((G2 | P2) + G2) ^ P2) >> warp) & 1u;  // carry into this warp (0 into the first)
+  unsigned c = (unsigned)((((unsigned long long)(Gw | Pw)) + Gw + cw) ^ Pw) >> lane & 1u;
+  unsigned d[4];
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    d[i] = u[i] + c;
+    c = (g[i] || (p[i] && c != 0u)) ? 1u : 0u;
+  }
+  const int k0 = 4 * t;
+  if (k0 >= words) return;
+  const int i0 = 4 * k0;  // first digit of this thread
+  if (i0 + 15 < nout && ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
+    *reinterpret_cast<uint4 *>(out + i0) = make_uint4(d[0], d[1], d[2], d[3]);
+  } else {
+#pragma unroll
+    for (int b = 0; b < 16; b++)
+      if (i0 + b < nout) out[i0 + b] = (uint8_t)(d[b >> 2] >> (8 * (b & 3)));
+  }
+  (void)s_wgp;
+}
+
+}  // namespace ivm

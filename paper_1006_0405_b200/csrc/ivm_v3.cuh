@@ -527,14 +527,14 @@ __device__ __forceinline__ void cert_flush(const CertAcc &acc, Cert3 &cs) {
 
 // final output of the last inverse pass: v = z^{-k} O, c_k = 2 Re v / m,
 // c_{k+m/2} = 2 Im v / m  (the folded radix-2 step)
-template <typename T, int M>
+template <typename T, int M, int QS = 0>
 __device__ __forceinline__ void emit_coeffs(const CI<T> &o, int k, const TwC<T> *__restrict__ tw, int twi,
                                             int n, int32_t *coef, CertAcc &acc, double *dump) {
   constexpr int N = 1 << M;
   const CI<T> v = rtmul<T, true>(ldg_twc(tw, twi), o);  // z^{-k} = conj(z^k)
   const T s = T(2) / T(N);  // exact power of two
-  certify_real(DR<T>::mul_rd(v.rl, s), DR<T>::mul_ru(v.rh, s), k, n, coef + k, acc, dump);
-  certify_real(DR<T>::mul_rd(v.il, s), DR<T>::mul_ru(v.ih, s), k + N / 2, n, coef + k + N / 2, acc, dump);
+  certify_real(DR<T>::mul_rd(v.rl, s), DR<T>::mul_ru(v.rh, s), k, n, coef + cpos<QS>(k), acc, dump);
+  certify_real(DR<T>::mul_rd(v.il, s), DR<T>::mul_ru(v.ih, s), k + N / 2, n, coef + cpos<QS>(k + N / 2), acc, dump);
   dump_prerot(dump, k, N, o, s);
 }
 
@@ -552,7 +552,7 @@ __device__ __forceinline__ void emit_fold(const CI<T> &o, int r, int k, int n, i
   dump_prerot(dump, k, N, o, s);
 }
 
-template <typename T, int M, int RK, bool WARP = false>
+template <typename T, int M, int RK, bool WARP = false, int QS = 0>
 __device__ __forceinline__ void inv_last(Buf<T> st, const TwC<T> *__restrict__ tw, int n, int32_t *coef,
                                          CertAcc &acc, double *dump, int tid = threadIdx.x) {
   using Gm = G3<M, RK>;
@@ -570,7 +570,7 @@ __device__ __forceinline__ void inv_last(Buf<T> st, const TwC<T> *__restrict__ t
 #pragma unroll
     for (int r = 0; r < Q; r++) {
       const int k = k0s[g] + L * r;
-      emit_coeffs<T, M>(v[g][r], k, tw, TWF + k, n, coef, acc, dump);
+      emit_coeffs<T, M, QS>(v[g][r], k, tw, TWF + k, n, coef, acc, dump);
     }
   }
 }
@@ -771,6 +771,7 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
   constexpr unsigned L16_BYTES = LAST16 ? sizeof(TwC<T>) * R * Gm::LASTL() : 0;
   constexpr unsigned SMF_BYTES = sizeof(TwC<T>) * Gm::SMF_ENT(), SMI_BYTES = sizeof(TwC<T>) * Gm::SMI_ENT();
   constexpr int RATIO = 2 * N / Gm::LASTL();
+  constexpr int QS = C::THREADS;  // coefficient layout of the 4-words-per-thread carry (cpos)
   // digits staged by bulk copies when every row is 16-byte aligned
   const bool staged =
       (n % 16 == 0) && ((reinterpret_cast<uintptr_t>(kp.a) | reinterpret_cast<uintptr_t>(kp.b)) % 16 == 0);
@@ -875,7 +876,7 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
 #pragma unroll
         for (int r = 0; r < R; r++) {
           const int k = k0 + pp.L * r;
-          emit_fold<T, M, RATIO>(v[r], r, k, n, coef + k, coef + k + N / 2, acc, dump);
+          emit_fold<T, M, RATIO>(v[r], r, k, n, coef + cpos<QS>(k), coef + cpos<QS>(k + N / 2), acc, dump);
         }
       } else {
         invR<T, R, false>(st, twb, pp, v, k0, nu);
@@ -885,7 +886,7 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
       }
       __syncthreads();
     }
-    if constexpr (!LAST16) inv_last<T, M, R>(st, tw, n, coef, acc, diag_dump(kp, pair, N));
+    if constexpr (!LAST16) inv_last<T, M, R, false, QS>(st, tw, n, coef, acc, diag_dump(kp, pair, N));
     IVM_PH(4);
     cert_flush(acc, cs);
     __syncthreads();
@@ -895,10 +896,10 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
       bulk_copy(twb, tw + Gm::tw_fwd(Gm::P.nf - 1), FL_BYTES, &tbar);
     }
     const bool certified = cs.ok != 0;
-    carry_store(coef, n, kp.prod + (size_t)pair * 2 * n, certified);
+    carry_store4<QS>(coef, n, kp.prod + (size_t)pair * 2 * n, certified);
     if (kp.coeffs) {
       int64_t *co = kp.coeffs + (size_t)pair * (2 * n - 1);
-      for (int i = threadIdx.x; i < 2 * n - 1; i += blockDim.x) co[i] = certified ? coef[i] : 0;
+      for (int i = threadIdx.x; i < 2 * n - 1; i += blockDim.x) co[i] = certified ? coef[cpos<QS>(i)] : 0;
     }
     if (threadIdx.x == 0) {
       kp.cert[pair] = certified ? 1 : 0;
