@@ -294,3 +294,126 @@ static __device__ __forceinline__ void carry_store4(const int32_t *coef, int n, 
 }
 
 }  // namespace ivm
+
+namespace ivm {
+
+// Chunked form of the four-words-per-thread carry (the cluster and group
+// kernels: every CTA carries 2C chunks of B/4 words, TPC = B/16 threads per
+// chunk, chunk carry-ins from a cluster/group-level adder in between).
+//   words(V): V = the six words 4t-2 .. 4t+3 of this thread (two below its own);
+//   seg_bits(): (generate | all-propagate << 1) of this thread's chunk when
+//     TPC <= 32 (a lane segment), of its warp when TPC > 32;
+//   chunk_bits(sw): TPC > 32, sw = the block's per-warp seg_bits (shared memory);
+//   lane_cin(cin, sw): carry into this thread's first word given the chunk's;
+//   digits(c, d): the four digit words.
+template <int TPC>
+struct Carry4 {
+  static_assert(TPC >= 2 && TPC <= 512 && (TPC & (TPC - 1)) == 0, "threads per chunk");
+  unsigned u[4];
+  unsigned gb, pb;  // bit i: generate / propagate of word i
+  unsigned Gw, Pw;  // the warp's ballots of the per-thread composites
+
+  __device__ __forceinline__ void words(const unsigned long long (&V)[6]) {
+    unsigned lo[6], hi[6], w[6], e[6];
+#pragma unroll
+    for (int j = 0; j < 6; j++) {
+      lo[j] = (unsigned)V[j];
+      hi[j] = (unsigned)(V[j] >> 32);
+    }
+#pragma unroll
+    for (int j = 1; j < 6; j++) {
+      w[j] = lo[j] + hi[j - 1];
+      e[j] = w[j] < lo[j] ? 1u : 0u;
+    }
+    gb = pb = 0u;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      u[i] = w[i + 2] + e[i + 1];
+      const bool g = e[i + 1] != 0u && w[i + 2] == 0xffffffffu;
+      const bool p = u[i] == 0xffffffffu && !g;
+      gb |= (g ? 1u : 0u) << i;
+      pb |= (p ? 1u : 0u) << i;
+    }
+    // the thread's composite over its 4 words: the same ballot adder on 4 bits
+    const bool G = ((((gb | pb) + gb) >> 4) & 1u) != 0u, P = pb == 15u;
+    Gw = __ballot_sync(0xffffffffu, G);
+    Pw = __ballot_sync(0xffffffffu, P);
+  }
+  __device__ __forceinline__ unsigned seg_bits() const {
+    if constexpr (TPC >= 32) {
+      const unsigned gen = (unsigned)(((unsigned long long)(Gw | Pw) + Gw) >> 32);
+      return gen | ((Pw == 0xffffffffu ? 1u : 0u) << 1);
+    } else {
+      constexpr unsigned MASK = (1u << TPC) - 1u;
+      const unsigned sh = (threadIdx.x & 31u) / TPC * TPC;
+      const unsigned Gs = (Gw >> sh) & MASK, Ps = (Pw >> sh) & MASK;
+      return ((((Gs | Ps) + Gs) >> TPC) & 1u) | ((Ps == MASK ? 1u : 0u) << 1);
+    }
+  }
+  // TPC > 32: fold the chunk's warps (first .. first + TPC/32 - 1) of sw, in word order
+  static __device__ __forceinline__ unsigned chunk_bits(const unsigned *sw) {
+    constexpr int WPC = TPC / 32;
+    const int first = (int)(threadIdx.x >> 5) / WPC * WPC;
+    unsigned g = 0u, a = 1u;
+#pragma unroll
+    for (int j = 0; j < WPC; j++) {
+      const unsigned b = sw[first + j];
+      g = (b & 1u) | (((b >> 1) & 1u) & g);
+      a &= (b >> 1) & 1u;
+    }
+    return g | (a << 1);
+  }
+  __device__ __forceinline__ unsigned lane_cin(unsigned cin, const unsigned *sw) const {
+    const unsigned lane = threadIdx.x & 31u;
+    if constexpr (TPC >= 32) {
+      unsigned cw = cin;  // through the chunk's warps below this one
+      if constexpr (TPC > 32) {
+        constexpr int WPC = TPC / 32;
+        const int wi = (int)(threadIdx.x >> 5) % WPC, first = (int)(threadIdx.x >> 5) - wi;
+        for (int j = 0; j < wi; j++) {
+          const unsigned b = sw[first + j];
+          cw = (b & 1u) | (((b >> 1) & 1u) & cw);
+        }
+      }
+      return (unsigned)(((((unsigned long long)(Gw | Pw)) + Gw + cw) ^ Pw) >> lane) & 1u;
+    } else {
+      constexpr unsigned MASK = (1u << TPC) - 1u;
+      const unsigned sh = lane / TPC * TPC;
+      const unsigned Gs = (Gw >> sh) & MASK, Ps = (Pw >> sh) & MASK;
+      return ((((Gs | Ps) + Gs + cin) ^ Ps) >> (lane - sh)) & 1u;
+    }
+  }
+  __device__ __forceinline__ void digits(unsigned c, unsigned (&d)[4]) const {
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      d[i] = u[i] + c;
+      c = ((gb >> i) & 1u) | (((pb >> i) & 1u) & c);
+    }
+  }
+};
+
+// the 16 digit bytes of words k0 .. k0+3 (digit 4 k0 on), clipped to nout
+__device__ __forceinline__ void store_words4(uint8_t *__restrict__ out, int k0, int nout, const unsigned (&d)[4]) {
+  const int i0 = 4 * k0;
+  if (i0 >= nout) return;
+  if (i0 + 15 < nout && ((reinterpret_cast<uintptr_t>(out + i0) & 15) == 0)) {
+    *reinterpret_cast<uint4 *>(out + i0) = make_uint4(d[0], d[1], d[2], d[3]);
+  } else {
+#pragma unroll
+    for (int b = 0; b < 16; b++)
+      if (i0 + b < nout) out[i0 + b] = (uint8_t)(d[b >> 2] >> (8 * (b & 3)));
+  }
+}
+
+// word value V = c0 + c1 2^8 + c2 2^16 + c3 2^24 of four coefficients (those at
+// global index >= nc are zero)
+__device__ __forceinline__ unsigned long long word_of(unsigned long long c0, unsigned long long c1,
+                                                      unsigned long long c2, unsigned long long c3, int i0, int nc) {
+  if (i0 >= nc) return 0ull;
+  c1 = i0 + 1 < nc ? c1 : 0ull;
+  c2 = i0 + 2 < nc ? c2 : 0ull;
+  c3 = i0 + 3 < nc ? c3 : 0ull;
+  return c0 + (c1 << 8) + (c2 << 16) + (c3 << 24);
+}
+
+}  // namespace ivm

@@ -268,7 +268,6 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
   constexpr int C = X::C, B = X::B, R = 8, NL = 8192, N = 1 << M;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Cert3 cs;
-  __shared__ CarrySeg seg;
   __shared__ unsigned s_chunk[2 * (1 << (M - 13))][2];  // this CTA's chunks: generate, all-propagate
   __shared__ unsigned s_cin[4];                         // carry into each of the 2C^2 chunks
   __shared__ __align__(8) unsigned long long tbar, dbar;
@@ -440,8 +439,8 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
         const int kl = (int)threadIdx.x + 512 * g, k0 = (int)crank * B + kl;
 #pragma unroll
         for (int r = 0; r < C; r++)
-          emit_fold<T, M, 4 * C>(v[g][r], r, k0 + 4096 * r, n, coefL + r * B + kl, coefL + (C + r) * B + kl, acc,
-                                 dump);
+          emit_fold<T, M, 4 * C>(v[g][r], r, k0 + 4096 * r, n, coefL + r * B + cpos<B / 16>(kl),
+                                 coefL + (C + r) * B + cpos<B / 16>(kl), acc, dump);
       }
     }
     cert_flush(acc, cs);
@@ -478,22 +477,49 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
     IVM_PH(8);
     const int ok = s_ok, bad = s_bad;
     const unsigned long long rad = s_rad;
-    // carry: coefficient chunk ch (B coefficients, B/4 words) lives in CTA ch mod C
-    // at local chunk ch / C, so each CTA carries its own 2C chunks, one team of
-    // 8/C warps per chunk; only the chunks' (generate, all-propagate) bits and
-    // two boundary words per chunk cross the cluster
-    constexpr int NCH = 2 * C, TWP = 16 / NCH, WB = B / 4, NCHT = 2 * C * C;
-    const int lc = (int)(threadIdx.x >> 5) / TWP, w0 = lc * TWP, ch = lc * C + (int)crank;
-    const int tt = (int)threadIdx.x - 32 * w0;  // thread index within the team
+    // carry: coefficient chunk ch (B coefficients, WB = B/4 words) lives in CTA ch mod C
+    // at local chunk ch / C (cpos layout inside the chunk), so each CTA carries its own
+    // 2C chunks with TPC = WB/4 threads per chunk and four words per thread
+    // (Carry4); only the chunks' (generate, all-propagate) bits and the two words
+    // below each chunk cross the cluster
+    constexpr int NCH = 2 * C, WB = B / 4, TPC = WB / 4, NCHT = 2 * C * C;
+    static_assert(NCH * TPC == 512, "one thread per four words");
+    const int lc = (int)threadIdx.x / TPC, tc = (int)threadIdx.x % TPC, ch = lc * C + (int)crank;
     const int words = (nout + 3) / 4;
-    const int kb = min(ch * WB, words), ke = min(kb + WB, words);
     uint8_t *out = kp.prod + (size_t)pair * nout;
-    const CoefCluster<M> src{(unsigned)__cvta_generic_to_shared(coefL)};
-    unsigned gen = 0u, allp = 1u;
-    if (ok) carry_seg_scan(src, nc, kb, ke, seg, gen, allp, w0, TWP);
-    if (tt == 0) {
-      s_chunk[lc][0] = gen;
-      s_chunk[lc][1] = allp;
+    __shared__ unsigned s_w[16];  // TPC > 32: per-warp (generate, all-propagate)
+    Carry4<TPC> cy;
+    if (ok) {
+      const unsigned cbase = (unsigned)__cvta_generic_to_shared(coefL);
+      unsigned long long V[6];
+#pragma unroll
+      for (int j = 0; j < 6; j++) {
+        const int wj = 4 * tc - 2 + j;  // word of this chunk (< 0: the chunk below)
+        const int gi = ch * B + 4 * wj;  // global index of its first coefficient
+        V[j] = 0ull;
+        if (wj >= 0) {
+          const int4 q = *reinterpret_cast<const int4 *>(coefL + lc * B + cpos<TPC>(4 * wj));
+          V[j] = word_of((unsigned)q.x, (unsigned)q.y, (unsigned)q.z, (unsigned)q.w, gi, nc);
+        } else if (ch > 0) {  // the last two words of chunk ch - 1 (CTA (ch-1) mod C)
+          const int pc = ch - 1;
+          const int4 q = dsm_ld_i4(dsm_map_addr(cbase + 4u * (unsigned)((pc / C) * B + cpos<TPC>(4 * (WB + wj))),
+                                                (unsigned)(pc % C)));
+          V[j] = word_of((unsigned)q.x, (unsigned)q.y, (unsigned)q.z, (unsigned)q.w, gi, nc);
+        }
+      }
+      cy.words(V);
+      unsigned cb;
+      if constexpr (TPC > 32) {
+        if ((threadIdx.x & 31u) == 0u) s_w[threadIdx.x >> 5] = cy.seg_bits();
+        __syncthreads();
+        cb = Carry4<TPC>::chunk_bits(s_w);
+      } else {
+        cb = cy.seg_bits();
+      }
+      if (tc == 0) {
+        s_chunk[lc][0] = cb & 1u;
+        s_chunk[lc][1] = cb >> 1;
+      }
     }
     IVM_PH(9);
     cluster_sync();  // (4) every chunk's generate / all-propagate published
@@ -513,24 +539,28 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
           P[w] = __ballot_sync(0xffffffffu, pq);
         }
         if (threadIdx.x == 0) {
-          unsigned long long cy = 0ull;
+          unsigned long long cyc = 0ull;
 #pragma unroll
           for (int w = 0; w < 4; w++) {
-            const unsigned long long S = (unsigned long long)(G[w] | P[w]) + G[w] + cy;
+            const unsigned long long S = (unsigned long long)(G[w] | P[w]) + G[w] + cyc;
             s_cin[w] = (unsigned)S ^ P[w];
-            cy = S >> 32;
+            cyc = S >> 32;
           }
         }
       }
       __syncthreads();
       const unsigned cin = (s_cin[ch >> 5] >> (ch & 31)) & 1u;
-      carry_seg_emit(src, nc, nout, kb, ke, seg, cin, out, w0, TWP);
+      unsigned d[4];
+      cy.digits(cy.lane_cin(cin, s_w), d);
+      const int k0 = ch * WB + 4 * tc;
+      if (k0 < words) store_words4(out, k0, nout, d);
     } else {
-      for (int i = 4 * kb + tt; i < min(4 * ke, nout); i += 32 * TWP) out[i] = 0;
+      for (int i = ch * B + 4 * tc; i < min(ch * B + B, nout); i += 4 * TPC)
+        for (int b = 0; b < 4 && i + b < nout; b++) out[i + b] = 0;
     }
     if (kp.coeffs) {
       int64_t *co = kp.coeffs + (size_t)pair * nc;
-      for (int i = 4 * kb + tt; i < min(4 * ke, nc); i += 32 * TWP) co[i] = ok ? (int64_t)src.one(i) : 0;
+      for (int l = tc; l < B && ch * B + l < nc; l += TPC) co[ch * B + l] = ok ? (int64_t)coefL[lc * B + cpos<TPC>(l)] : 0;
     }
     if (crank == 0 && threadIdx.x == 0) {
       kp.cert[pair] = ok ? 1 : 0;
