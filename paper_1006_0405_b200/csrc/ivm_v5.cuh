@@ -273,7 +273,6 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
   constexpr int C2 = TWO ? C / 8 : 1;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Cert3 cs;
-  __shared__ CarrySeg seg;
   __shared__ __align__(8) unsigned long long tbar;
   Buf<T> st{reinterpret_cast<V *>(smem), reinterpret_cast<V *>(smem) + GL::CAP};
   TwC<T> *twb = reinterpret_cast<TwC<T> *>(smem + CF::STATE_BYTES);
@@ -425,7 +424,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
         const int kl = (int)threadIdx.x + 512 * g, k0 = (int)crank * B + kl;
 #pragma unroll
         for (int r = 0; r < C; r++)
-          emit_tab<T, M>(v[g][r], fold[2 * r], k0 + 4096 * r, n, coefL + r * B + kl, coefL + (C + r) * B + kl, acc, dump);
+          emit_tab<T, M>(v[g][r], fold[2 * r], k0 + 4096 * r, n, coefL + r * B + cpos<B / 16>(kl), coefL + (C + r) * B + cpos<B / 16>(kl), acc, dump);
       }
     } else {
       // gather + input twiddles: y_q(kl) -> state[q B + kl]
@@ -474,7 +473,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
 #pragma unroll
             for (int r2 = 0; r2 < C2; r2++) {
               const int r = r1 + 8 * r2, k = k0 + 4096 * r;
-              emit_tab<T, M>(v[r2], fold[2 * r], k, n, coefL + r * B + kl, coefL + (C + r) * B + kl, acc, dump);
+              emit_tab<T, M>(v[r2], fold[2 * r], k, n, coefL + r * B + cpos<B / 16>(kl), coefL + (C + r) * B + cpos<B / 16>(kl), acc, dump);
             }
           }
         } else {
@@ -494,7 +493,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
 #pragma unroll
             for (int r2 = 0; r2 < C2; r2++) {
               const int r = r1 + 8 * r2, k = k0 + 4096 * r;
-              emit_tab<T, M>(v[g2][r2], fold[2 * r], k, n, coefL + r * B + kl, coefL + (C + r) * B + kl, acc, dump);
+              emit_tab<T, M>(v[g2][r2], fold[2 * r], k, n, coefL + r * B + cpos<B / 16>(kl), coefL + (C + r) * B + cpos<B / 16>(kl), acc, dump);
             }
           }
         }
@@ -507,12 +506,13 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
     // teams: one warp per chunk and NCH / 16 rounds (C >= 8), else one round of
     // 16 / NCH warps per chunk
     constexpr int NCH = 2 * C, NCHT = 2 * C * C, WB = B / 4;
-    constexpr int TWP = NCH >= 16 ? 1 : 16 / NCH, ROUNDS = NCH >= 16 ? NCH / 16 : 1;
+    constexpr int TPC = WB / 4;  // threads per chunk, four words each (Carry4)
+    static_assert(NCH * TPC == 512, "one thread per four words");
     long long *bnd = g.bnd + (size_t)gi * NCHT * 8;
     uint8_t *bits = g.bits + (size_t)gi * NCHT;
     for (int e = (int)threadIdx.x; e < NCH * 8; e += blockDim.x) {  // boundary words of the own chunks
       const int lc = e / 8, ch = lc * C + (int)crank;
-      bnd[(size_t)ch * 8 + (e % 8)] = coefL[lc * B + B - 8 + (e % 8)];
+      bnd[(size_t)ch * 8 + (e % 8)] = coefL[lc * B + cpos<B / 16>(B - 8 + (e % 8))];
     }
     if (threadIdx.x == 0) {
       link[crank * 8 + 0] = (unsigned)cs.ok;
@@ -560,17 +560,40 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
     IVM_PH(8);
     const int ok = s_ok, bad = s_bad;
     const unsigned long long rad = s_rad;
-    const int words = (nout + 3) / 4, warp = (int)threadIdx.x >> 5;
+    const int words = (nout + 3) / 4;
     uint8_t *out = kp.prod + (size_t)pair * nout;
-    const int w0 = warp / TWP * TWP;  // first warp of this thread's team
-#pragma unroll 1
-    for (int rd = 0; rd < ROUNDS; rd++) {
-      const int lc = rd * 16 + warp / TWP, ch = lc * C + (int)crank;
-      const int kb = min(ch * WB, words), ke = min(kb + WB, words);
-      const ChunkSrc src{coefL + lc * B, s_prev[lc], ch * B};
-      unsigned gn = 0u, ap = 1u;
-      if (ok) carry_seg_scan(src, nc, kb, ke, seg, gn, ap, w0, TWP);
-      if ((int)threadIdx.x == 32 * w0) bits[ch] = (uint8_t)(gn | (ap << 1));
+    // thread t carries words 4 tc .. 4 tc + 3 of its chunk lc (cpos layout); the two
+    // words below a chunk's first come from s_prev (the chunk below, any CTA)
+    const int lc = (int)threadIdx.x / TPC, tc = (int)threadIdx.x % TPC, ch = lc * C + (int)crank;
+    __shared__ unsigned s_w[16];  // TPC > 32: per-warp (generate, all-propagate)
+    Carry4<TPC> cy;
+    if (ok) {
+      unsigned long long V[6];
+#pragma unroll
+      for (int j = 0; j < 6; j++) {
+        const int wj = 4 * tc - 2 + j, gi0 = ch * B + 4 * wj;
+        unsigned long long c[4];
+        if (wj >= 0) {
+          const longlong2 *q = reinterpret_cast<const longlong2 *>(coefL + lc * B + cpos<TPC>(4 * wj));
+          const longlong2 x = q[0], y = q[1];
+          c[0] = (unsigned long long)x.x, c[1] = (unsigned long long)x.y;
+          c[2] = (unsigned long long)y.x, c[3] = (unsigned long long)y.y;
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; e++) c[e] = (unsigned long long)s_prev[lc][4 * (wj + 2) + e];
+        }
+        V[j] = (wj >= 0 || ch > 0) ? word_of(c[0], c[1], c[2], c[3], gi0, nc) : 0ull;
+      }
+      cy.words(V);
+      unsigned cb;
+      if constexpr (TPC > 32) {
+        if ((threadIdx.x & 31u) == 0u) s_w[threadIdx.x >> 5] = cy.seg_bits();
+        __syncthreads();
+        cb = Carry4<TPC>::chunk_bits(s_w);
+      } else {
+        cb = cy.seg_bits();
+      }
+      if (tc == 0) bits[ch] = (uint8_t)cb;
     }
     IVM_PH(9);
     gsync(ctr, C, gen);  // (3) every chunk's generate / all-propagate visible
@@ -618,26 +641,19 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
         }
       }
       __syncthreads();
-#pragma unroll 1
-      for (int rd = 0; rd < ROUNDS; rd++) {
-        const int lc = rd * 16 + warp / TWP, ch = lc * C + (int)crank;
-        const int kb = min(ch * WB, words), ke = min(kb + WB, words);
-        const ChunkSrc src{coefL + lc * B, s_prev[lc], ch * B};
-        // a one-warp team: the carry into the warp is the chunk's carry-in whatever
-        // the (stale) per-warp bits in seg say; larger teams use the scan's bits
-        carry_seg_emit(src, nc, nout, kb, ke, seg, s_cin[lc], out, w0, TWP);
-      }
+      unsigned d[4];
+      cy.digits(cy.lane_cin(s_cin[lc], s_w), d);
+      const int k0 = ch * WB + 4 * tc;
+      if (k0 < words) store_words4(out, k0, nout, d);
     } else {
-      for (int lc = 0; lc < NCH; lc++) {
-        const int ch = lc * C + (int)crank, kb = min(ch * WB, words), ke = min(kb + WB, words);
-        for (int i = 4 * kb + (int)threadIdx.x; i < min(4 * ke, nout); i += blockDim.x) out[i] = 0;
-      }
+      for (int i = ch * B + 4 * tc; i < min(ch * B + B, nout); i += 4 * TPC)
+        for (int b = 0; b < 4 && i + b < nout; b++) out[i + b] = 0;
     }
     if (kp.coeffs) {
       int64_t *co = kp.coeffs + (size_t)pair * nc;
       for (int e = (int)threadIdx.x; e < NCH * B; e += blockDim.x) {
-        const int lc = e / B, i = (lc * C + (int)crank) * B + e % B;
-        if (i < nc) co[i] = ok ? coefL[e] : 0;
+        const int lc2 = e / B, i = (lc2 * C + (int)crank) * B + e % B;
+        if (i < nc) co[i] = ok ? coefL[lc2 * B + cpos<B / 16>(e % B)] : 0;
       }
     }
     __syncthreads();  // coefficients read before the next pair's state / table writes
