@@ -244,6 +244,49 @@ __device__ __forceinline__ void cross_fwd(const uint8_t *__restrict__ dig, int n
   }
 }
 
+// The cross pass fused with local pass 1 (the cluster kernel): thread t's cross
+// sums are the columns t + 512 j (j < 8) of row `crank`, which are exactly the
+// inputs of its local pass-1 task (k0 = 0, nu = t, Sp = 512), so they stay in
+// registers: the pass-1 twiddles (one per q, the same for every thread) and the
+// 8-point DFT follow at once, with no shared-memory round trip of the cross row.
+// Odd roles take the conjugate (the mirrored row), as cross_fwd's st_conj does.
+template <typename T, int M>
+__device__ __forceinline__ void cross_pass1(const uint8_t *__restrict__ dig, int n, const CI<T> *theta, unsigned crank,
+                                            const TwC<T> *twb, const PassRT &pp, CI<T> (&v)[8]) {
+  constexpr int C = G4<M>::C;
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int j = 0; j < 8; j++) v[j] = CI<T>{T(0), T(0), T(0), T(0)};
+#pragma unroll
+  for (int q = 0; q < C; q++) {
+    const CI<T> th = theta[q];
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      const int idx = t + 512 * j + 4096 * q;
+      const T x = idx < n ? digit_val<T>((unsigned)dig[idx]) : T(0);
+      v[j].rl = DR<T>::fma_rd(x, th.rl, v[j].rl);
+      v[j].rh = DR<T>::fma_ru(x, th.rh, v[j].rh);
+      v[j].il = DR<T>::fma_rd(x, th.il, v[j].il);
+      v[j].ih = DR<T>::fma_ru(x, th.ih, v[j].ih);
+    }
+  }
+  if (crank & 1u) {
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      const T il = v[j].il;
+      v[j].il = TB<T>::neg(v[j].ih);
+      v[j].ih = TB<T>::neg(il);
+    }
+  }
+  // local pass 1: row k0 = 0, twiddle of input q at pp.tw + (q - 1) (angles < pi/2 for q <= 4)
+#pragma unroll
+  for (int q = 1; q < 8; q++) {
+    const TwC<T> w = twb[pp.tw + q - 1];
+    v[q] = (2 * q <= 8) ? rtmul<T, false, false>(w, v[q]) : rtmul<T, false, true>(w, v[q]);
+  }
+  cdft<T, 8, false>(v);
+}
+
 template <typename T, int M> struct Cfg4 {
   using GL = G3<13, 8>;
   static constexpr int THREADS = 512;
@@ -324,8 +367,31 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
 #pragma unroll 1
     for (int op = 0; op < 2; op++) {
       if (staged) mbar_wait(&dbar, (unsigned)op);
-      cross_fwd<T, M>(staged ? sdig : (op == 0 ? kp.a : kp.b) + (size_t)pair * n, n, st, theta, crank,
-                      op == 0 && it > 0, !staged);
+      if (staged) {  // the cross pass fused with local pass 1, stored in the pass-2 layout
+        const PassRT pp = pick_fwd4<M>(0);
+        CI<T> v[R];
+        cross_pass1<T, M>(sdig, n, theta, crank, twb, pp, v);
+        if (op == 0 && it > 0) cluster_wait();  // the previous pair's remote reads of this state are done
+        const int nu = (int)threadIdx.x;
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+          if (2 * r < R) st.st(sidx(pp.L * r, nu, pp.RSo, pp.SWo), v[r]);
+          else st.st_conj(sidx(R * pp.L - 1 - pp.L * r, nu, pp.RSo, pp.SWo), v[r]);
+        }
+      } else {  // digits from L2 (word loads): the cross row through shared memory, then pass 1
+        cross_fwd<T, M>((op == 0 ? kp.a : kp.b) + (size_t)pair * n, n, st, theta, crank, op == 0 && it > 0, true);
+        __syncthreads();
+        const PassRT pp = pick_fwd4<M>(0);
+        CI<T> v[R];
+        int k0, nu;
+        fwdR<T, R>(st, twb, pp, v, k0, nu);
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+          if (2 * r < R) st.st(sidx(k0 + pp.L * r, nu, pp.RSo, pp.SWo), v[r]);
+          else st.st_conj(sidx(R * pp.L - 1 - k0 - pp.L * r, nu, pp.RSo, pp.SWo), v[r]);
+        }
+      }
       if (op == 0 && it > 0 && threadIdx.x == 0) {
         // this pair's forward-last table into the swap buffer: the cluster wait in
         // cross_fwd ordered every remote read of the previous coefficients before it
@@ -347,7 +413,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
         }
       }
 #pragma unroll 1
-      for (int i = 0; i < 4; i++) {
+      for (int i = 1; i < 4; i++) {
         const PassRT pp = pick_fwd4<M>(i);
         CI<T> v[R];
         int k0, nu;
