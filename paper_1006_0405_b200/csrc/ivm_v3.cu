@@ -37,6 +37,14 @@ static int v3_tables_impl(const F *w2N /* [2N][4] */, F *out) {
   const long N2 = 2L * N;
   bool ok = true;
   auto put = [&](int idx, long e) { ok = ok && compact(w2N + 4L * (((e % N2) + N2) % N2), out + 2L * idx); };
+  // the last inverse pass's tables also carry the exact scale 2/m of P:97 (a power of
+  // two: every product, sum and rounding of that pass scales exactly, so the
+  // coefficients are bit-identical to scaling them afterwards)
+  auto put_s = [&](int idx, long e) {
+    put(idx, e);
+    out[2L * idx] *= (F)2 / (F)N;
+    out[2L * idx + 1] *= (F)2 / (F)N;
+  };
   for (int p = 1; p < P.nf; p++) {  // forward: w_{2LR}^{q(2k0+1)} = w_{2N}^{q(2k0+1)S'}
     const int R = P.f[p], L = v3::fL(P, p), Sp = N / (L * R);
     for (int q = 1; q < R; q++)
@@ -50,14 +58,14 @@ static int v3_tables_impl(const F *w2N /* [2N][4] */, F *out) {
         else put(Gm::tw_inv(p) + (q - 1) * L + k0, 2L * (Q - q) * k0 * Sp);
       }
   }
-  for (int k = 0; k < N / 2; k++) put(Gm::tw_fin() + k, k);  // z^k (conj'd in-kernel)
+  for (int k = 0; k < N / 2; k++) put_s(Gm::tw_fin() + k, k);  // (2/m) z^k (conj'd in-kernel)
   if (Gm::LAST16) {  // last inverse pass (radix RK) with z^{-k0} folded in: [RK][L]
     const int p = P.ni - 1, Q = P.q[p], L = v3::iL(P, p), Sp = N / (L * Q);
     for (int q = 0; q < Q; q++)
       for (int k0 = 0; k0 < L; k0++) {
         // direct (q < 8): conj(u) with u = w_{LQ}^{q k0} z^{k0}; mirror: w_{LQ}^{(Q-q) k0} z^{-k0}
         const long e = (2 * q < Q) ? (long)k0 * (2L * q * Sp + 1) : (long)k0 * (2L * (Q - q) * Sp - 1);
-        put(Gm::tw_l16() + q * L + k0, e);
+        put_s(Gm::tw_l16() + q * L + k0, e);
       }
   }
   return ok ? Gm::tw_total() : -4;

@@ -480,9 +480,9 @@ __device__ __forceinline__ void certify_real(T lo, T hi, int i, int n, D *dst, C
   const double l = (double)lo, h = (double)hi;
   const double cl = ceil(l);
   const bool ok = cl == floor(h);
-  if (acc.radius) {
-    const double rad = __dmul_ru(__dadd_ru(h, -l), 0.5);
-    acc.rad = (rad <= acc.rad) ? acc.rad : rad;  // NaN propagates (comparison false)
+  if (acc.radius) {  // the width RU(h - l); halved (exactly) once, in cert_flush
+    const double wd = __dadd_ru(h, -l);
+    acc.rad = (wd <= acc.rad) ? acc.rad : wd;  // NaN propagates (comparison false)
   }
   *dst = ok ? (D)cl : (D)0;
   if (!ok) {
@@ -510,7 +510,7 @@ __device__ __forceinline__ void dump_prerot(double *dump, int k, int N, const CI
 __device__ __forceinline__ void cert_flush(const CertAcc &acc, Cert3 &cs) {
   const int ok = __reduce_and_sync(0xffffffffu, (unsigned)acc.ok);
   const int bad = (int)__reduce_min_sync(0xffffffffu, (unsigned)acc.bad);
-  double rad = acc.rad;
+  double rad = acc.rad * 0.5;  // radius = width / 2 (exact)
   for (int o = 16; o; o >>= 1) {
     const double r2 = __shfl_xor_sync(0xffffffffu, rad, o);
     rad = (r2 <= rad) ? rad : r2;
@@ -531,11 +531,11 @@ template <typename T, int M, int QS = 0>
 __device__ __forceinline__ void emit_coeffs(const CI<T> &o, int k, const TwC<T> *__restrict__ tw, int twi,
                                             int n, int32_t *coef, CertAcc &acc, double *dump) {
   constexpr int N = 1 << M;
-  const CI<T> v = rtmul<T, true>(ldg_twc(tw, twi), o);  // z^{-k} = conj(z^k)
-  const T s = T(2) / T(N);  // exact power of two
-  certify_real(DR<T>::mul_rd(v.rl, s), DR<T>::mul_ru(v.rh, s), k, n, coef + cpos<QS>(k), acc, dump);
-  certify_real(DR<T>::mul_rd(v.il, s), DR<T>::mul_ru(v.ih, s), k + N / 2, n, coef + cpos<QS>(k + N / 2), acc, dump);
-  dump_prerot(dump, k, N, o, s);
+  // (2/m) z^{-k} = conj of the table entry: the scale of P:97 is in the table
+  const CI<T> v = rtmul<T, true>(ldg_twc(tw, twi), o);
+  certify_real(v.rl, v.rh, k, n, coef + cpos<QS>(k), acc, dump);
+  certify_real(v.il, v.ih, k + N / 2, n, coef + cpos<QS>(k + N / 2), acc, dump);
+  dump_prerot(dump, k, N, o, T(1));
 }
 
 // folded variant: the input twiddles already carried z^{-k0}; the remaining
@@ -545,11 +545,10 @@ template <typename T, int M, int RATIO>
 __device__ __forceinline__ void emit_fold(const CI<T> &o, int r, int k, int n, int32_t *d0, int32_t *d1,
                                           CertAcc &acc, double *dump) {
   constexpr int N = 1 << M;
-  const CI<T> v = ctw<T, true>(o, r, RATIO);
-  const T s = T(2) / T(N);
-  certify_real(DR<T>::mul_rd(v.rl, s), DR<T>::mul_ru(v.rh, s), k, n, d0, acc, dump);
-  certify_real(DR<T>::mul_rd(v.il, s), DR<T>::mul_ru(v.ih, s), k + N / 2, n, d1, acc, dump);
-  dump_prerot(dump, k, N, o, s);
+  const CI<T> v = ctw<T, true>(o, r, RATIO);  // (the input twiddles carried the scale 2/m)
+  certify_real(v.rl, v.rh, k, n, d0, acc, dump);
+  certify_real(v.il, v.ih, k + N / 2, n, d1, acc, dump);
+  dump_prerot(dump, k, N, o, T(1));
 }
 
 template <typename T, int M, int RK, bool WARP = false, int QS = 0>

@@ -73,6 +73,8 @@ template <typename F, int M> static int v4_tables_impl(const F *w2N /* [2m][4] *
         const long k0 = (long)c * B + kl;
         const long e = (2 * q < C) ? k0 * (2 * q * Sp + 1) : k0 * (2 * (C - q) * Sp - 1);
         put(X::XINV(c) + q * B + kl, e);
+        out[2L * (X::XINV(c) + q * B + kl)] *= (F)2 / (F)N;  // the exact scale 2/m of P:97
+        out[2L * (X::XINV(c) + q * B + kl) + 1] *= (F)2 / (F)N;
       }
     const int r = (c % 2 == 0) ? c / 2 : (2 * C - 1 - c) / 2;
     for (int q = 0; q < C; q++) {

@@ -253,11 +253,10 @@ template <typename T, int M>
 __device__ __forceinline__ void emit_tab(const CI<T> &o, const TwC<T> &w, int k, int n, long long *d0,
                                          long long *d1, CertAcc &acc, double *dump) {
   constexpr int N = 1 << M;
-  const CI<T> v = rtmul<T, true, false>(w, o);
-  const T s = T(2) / T(N);
-  certify_real(DR<T>::mul_rd(v.rl, s), DR<T>::mul_ru(v.rh, s), k, n, d0, acc, dump);
-  certify_real(DR<T>::mul_rd(v.il, s), DR<T>::mul_ru(v.ih, s), k + N / 2, n, d1, acc, dump);
-  dump_prerot(dump, k, N, o, s);
+  const CI<T> v = rtmul<T, true, false>(w, o);  // (the input twiddles carried the scale 2/m)
+  certify_real(v.rl, v.rh, k, n, d0, acc, dump);
+  certify_real(v.il, v.ih, k + N / 2, n, d1, acc, dump);
+  dump_prerot(dump, k, N, o, T(1));
 }
 
 // QB: the cross pass skips its zero-padding terms in groups of 8 (host picks it

@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v6_kernel(KParams kp) {
       }
       if (tid == 0) {
         kp.cert[pair] = certified ? 1 : 0;
-        if (kp.max_radius) kp.max_radius[pair] = acc.rad;
+        if (kp.max_radius) kp.max_radius[pair] = acc.rad * 0.5;  // (acc tracks the width)
         if (kp.first_bad) kp.first_bad[pair] = certified ? -1 : acc.bad;
       }
     }
