@@ -459,13 +459,15 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
       if (i == 2) mbar_wait(&tbar, par ^ 1u);
       invR<T, R, false>(st, twb, pp, v, k0, nu);
       __syncthreads();
+      if (i == 2 && threadIdx.x == 0) {
+        // every read of the pass-3 table is done: the last inverse pass table (this
+        // role's rows) streams in while pass 3 stores and the cluster synchronises
+        mbar_expect(&tbar, EB * 4096);
+        bulk_copy(twb + X::S_SWAP, tw + X::XINV(crank), EB * 4096, &tbar);
+      }
 #pragma unroll
       for (int r = 0; r < R; r++) st.st(sidx(k0 + pp.L * r, nu, pp.RSo, pp.SWo), v[r]);
       __syncthreads();
-    }
-    if (threadIdx.x == 0) {  // last inverse pass table (this role's rows)
-      mbar_expect(&tbar, EB * 4096);
-      bulk_copy(twb + X::S_SWAP, tw + X::XINV(crank), EB * 4096, &tbar);
     }
     IVM_PH(4);
     cluster_sync();  // (1) every CTA's column of the 4096 rows is in its shared memory
@@ -488,6 +490,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
       }
       // (no cluster barrier here: the coefficients do not overwrite the state)
       mbar_wait(&tbar, par);
+      IVM_PH(12);
 #pragma unroll
       for (int g = 0; g < G; g++) {
         const int kl = (int)threadIdx.x + 512 * g;
@@ -499,6 +502,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
         cdft<T, C, true>(v[g]);
       }
       __syncthreads();  // every twiddle read: the swap buffer takes the coefficients
+      IVM_PH(13);
       double *dump = diag_dump(kp, pair, N);
 #pragma unroll
       for (int g = 0; g < G; g++) {

@@ -25,8 +25,9 @@ NAMES = {
     "v3": ["first pass a", "passes a", "first pass b", "passes b + pointwise + inv0", "inverse passes + emit",
            "cert flush", "carry + store"],
     "v4": ["cross a (+cluster wait)", "passes a", "cross b", "passes b + pointwise + inv0", "inverse local passes",
-           "cluster sync 1", "last pass (DSMEM) + emit", "cluster sync 3", "cert read", "carry scan",
-           "cluster sync 4", "carry emit"],
+           "cluster sync 1", "last pass: emit", "cluster sync 3", "cert read", "carry scan",
+           "cluster sync 4", "carry emit", "last pass: DSMEM loads + table wait",
+           "last pass: twiddles + DFT (load stalls)"],
     "v5": ["cross a", "passes a", "cross b", "passes b + pointwise + inv0", "inverse local passes + xch",
            "group barrier 1", "last pass (L2) + emit", "boundary + group barrier 2", "cert + prev fetch",
            "carry scan", "group barrier 3", "carry emit + tail"],
