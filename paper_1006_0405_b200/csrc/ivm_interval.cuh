@@ -166,4 +166,31 @@ __device__ __forceinline__ CI<T> cmul(const CI<T> &z, const CI<T> &w) {
   return t;
 }
 
+// Pointwise product with a single-sign fast path.  When no component of z or w
+// straddles zero (the sign bits of each lower and upper endpoint agree; -0 counts
+// as negative, so [-0, x] takes the general path), the exact argmin / argmax pair
+// of a real product x*y follows from the two signs alone:
+//   lo = (y < 0 ? xh : xl) * (x < 0 ? yh : yl),  hi = (y < 0 ? xl : xh) * (x < 0 ? yl : yh),
+// i.e. four predicates (the signs of z.re, z.im, w.re, w.im) and 16 double selects for
+// the complex product instead of cmul's nine-case classes; the FMA fusion and the
+// rounding are cmul's, so the result is bit-identical.  Anything else goes to cmul.
+template <typename T> __device__ __forceinline__ unsigned sgnw(T x);
+template <> __device__ __forceinline__ unsigned sgnw<double>(double x) { return (unsigned)__double2hiint(x); }
+template <> __device__ __forceinline__ unsigned sgnw<float>(float x) { return (unsigned)__float_as_int(x); }
+
+template <typename T>
+__device__ __forceinline__ CI<T> cmul_ss(const CI<T> &z, const CI<T> &w) {
+  const unsigned a = sgnw(z.rl), b = sgnw(z.rh), c = sgnw(z.il), d = sgnw(z.ih);
+  const unsigned e = sgnw(w.rl), f = sgnw(w.rh), g = sgnw(w.il), h = sgnw(w.ih);
+  if ((int)((a ^ b) | (c ^ d) | (e ^ f) | (g ^ h)) < 0) return cmul(z, w);
+  const bool zr = (int)a < 0, zi = (int)c < 0, wr = (int)e < 0, wi = (int)g < 0;
+  CI<T> t;
+  // re = z.re w.re - z.im w.im ; im = z.re w.im + z.im w.re
+  t.rl = DR<T>::fma_rd(-(wi ? z.il : z.ih), zi ? w.il : w.ih, DR<T>::mul_rd(wr ? z.rh : z.rl, zr ? w.rh : w.rl));
+  t.rh = DR<T>::fma_ru(-(wi ? z.ih : z.il), zi ? w.ih : w.il, DR<T>::mul_ru(wr ? z.rl : z.rh, zr ? w.rl : w.rh));
+  t.il = DR<T>::fma_rd(wr ? z.ih : z.il, zi ? w.rh : w.rl, DR<T>::mul_rd(wi ? z.rh : z.rl, zr ? w.ih : w.il));
+  t.ih = DR<T>::fma_ru(wr ? z.il : z.ih, zi ? w.rl : w.rh, DR<T>::mul_ru(wi ? z.rl : z.rh, zr ? w.il : w.ih));
+  return t;
+}
+
 }  // namespace ivm

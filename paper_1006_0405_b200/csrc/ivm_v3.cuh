@@ -845,7 +845,7 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
           for (int r = 0; r < R; r++) {
             const CI<T> a = an;
             if (r + 1 < R) an = A.ld((r + 1) * (pp.L >> 1) + k0);
-            v[r] = cmul(a, v[r]);
+            v[r] = cmul_ss(a, v[r]);
           }
           cdft<T, R, true>(v);
           __syncthreads();
