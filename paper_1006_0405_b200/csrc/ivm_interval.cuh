@@ -178,11 +178,18 @@ template <typename T> __device__ __forceinline__ unsigned sgnw(T x);
 template <> __device__ __forceinline__ unsigned sgnw<double>(double x) { return (unsigned)__double2hiint(x); }
 template <> __device__ __forceinline__ unsigned sgnw<float>(float x) { return (unsigned)__float_as_int(x); }
 
+// (the general product out of line: the cold straddle path keeps its registers
+// out of the hot passes' allocation)
 template <typename T>
+__device__ __noinline__ CI<T> cmul_cold(const CI<T> z, const CI<T> w) {
+  return cmul(z, w);
+}
+
+template <typename T, bool COLD_CALL = false>
 __device__ __forceinline__ CI<T> cmul_ss(const CI<T> &z, const CI<T> &w) {
   const unsigned a = sgnw(z.rl), b = sgnw(z.rh), c = sgnw(z.il), d = sgnw(z.ih);
   const unsigned e = sgnw(w.rl), f = sgnw(w.rh), g = sgnw(w.il), h = sgnw(w.ih);
-  if ((int)((a ^ b) | (c ^ d) | (e ^ f) | (g ^ h)) < 0) return cmul(z, w);
+  if ((int)((a ^ b) | (c ^ d) | (e ^ f) | (g ^ h)) < 0) return COLD_CALL ? cmul_cold(z, w) : cmul(z, w);
   const bool zr = (int)a < 0, zi = (int)c < 0, wr = (int)e < 0, wi = (int)g < 0;
   CI<T> t;
   // re = z.re w.re - z.im w.im ; im = z.re w.im + z.im w.re

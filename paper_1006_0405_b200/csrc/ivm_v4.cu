@@ -82,6 +82,16 @@ template <typename F, int M> static int v4_tables_impl(const F *w2N /* [2m][4] *
       memcpy(out + 2L * (X::TH(c) + 2 * q), w2N + 4L * e, 4 * sizeof(F));  // full interval
     }
   }
+  for (int c = 0; c < C; c++) {  // TH1: w_j theta_q (odd roles: w_j conj(theta_q)), full intervals
+    const int r = (c % 2 == 0) ? c / 2 : (2 * C - 1 - c) / 2;
+    for (int j = 0; j < 8; j++)
+      for (int q = 0; q < C; q++) {
+        const long ew = (long)j * (2 * c + 1) * 512;  // local pass 1, kappa = 0: k = c
+        const long et = (long)q * (1 + 4 * r) * (N / (2 * C));
+        const long e = (((ew + (c % 2 == 0 ? et : -et)) % N2) + N2) % N2;
+        memcpy(out + 2L * (X::TH1(c) + 2 * (j * C + q)), w2N + 4L * e, 4 * sizeof(F));
+      }
+  }
   for (int j = 0; j < C; j++) {  // compact upper-half roots: w_C^j (2j <= C) or w_C^{C-j}; z^{4096 j}
     put(X::S2 + 2 * j, (long)(2 * j <= C ? j : C - j) * (N2 / C));
     put(X::FO + 2 * j, (long)j * 4096);

@@ -57,7 +57,11 @@ template <int M> struct G4 {
   //           int8 [4 operands s][8 columns][32 q] (see cross_tc in ivm_v5.cuh); 64 C
   //           entries of 16 B (filled for fp64 only)
   static constexpr int LIMB = FO + 2 * C;
-  static constexpr int TOTAL = LIMB + 64 * C;
+  //   TH1(c): role c, the cross pass fused with local pass 1 (cross_pass1): [8 j][C q]
+  //           full intervals of w_j theta_q (odd roles: w_j conj(theta_q)), w_j the
+  //           pass-1 twiddle of input j -- one root of unity each, optimally enclosed
+  __host__ __device__ static constexpr int TH1(int c) { return LIMB + 64 * C + 16 * C * c; }
+  static constexpr int TOTAL = LIMB + 64 * C + 16 * C * C;
   // shared-memory twiddle area (entries)
   static constexpr int S_SWAP = 0;          // 4096: forward-last -> inverse pass 3 -> last inverse pass
   static constexpr int S_MF = 4096;         // forward passes 1..3 (511 entries + 1 pad)
@@ -65,7 +69,8 @@ template <int M> struct G4 {
   static constexpr int S_TH = 4096 + 1016;  // theta (2C entries)
   static constexpr int S_S2 = S_TH + 2 * C;  // v5 only
   static constexpr int S_FO = S_S2 + 2 * C;  // v5 only
-  static constexpr int S_ENT = S_TH + 2 * C;  // v4 (v5: S_FO + 2 C)
+  static constexpr int S_TH1 = S_FO + 2 * C;  // v4: TH1 of this role (16 C entries)
+  static constexpr int S_ENT = S_TH1 + 16 * C;  // v4 (v5: S_FO + 2 C)
   static constexpr int FLAST = 3584, MF_ENT = 512, MI_ENT = 504;
 };
 
@@ -250,18 +255,22 @@ __device__ __forceinline__ void cross_fwd(const uint8_t *__restrict__ dig, int n
 // registers: the pass-1 twiddles (one per q, the same for every thread) and the
 // 8-point DFT follow at once, with no shared-memory round trip of the cross row.
 // Odd roles take the conjugate (the mirrored row), as cross_fwd's st_conj does.
+// The pass-1 twiddle of input j and the cross coefficients combine into one root
+// of unity per (j, q) (table TH1), so the twiddle products vanish: input j of
+// thread t's pass-1 task is sum_q Theta[j][q] x[t + 512 j + 4096 q], four directed
+// FMAs per term (x >= 0 is a point), then the 8-point DFT.
 template <typename T, int M>
-__device__ __forceinline__ void cross_pass1(const uint8_t *__restrict__ dig, int n, const CI<T> *theta, unsigned crank,
-                                            const TwC<T> *twb, const PassRT &pp, CI<T> (&v)[8]) {
+__device__ __forceinline__ void cross_pass1(const uint8_t *__restrict__ dig, int n, const CI<T> *__restrict__ th1,
+                                            CI<T> (&v)[8]) {
   constexpr int C = G4<M>::C;
   const int t = threadIdx.x;
 #pragma unroll
   for (int j = 0; j < 8; j++) v[j] = CI<T>{T(0), T(0), T(0), T(0)};
 #pragma unroll
-  for (int q = 0; q < C; q++) {
-    const CI<T> th = theta[q];
+  for (int j = 0; j < 8; j++) {
 #pragma unroll
-    for (int j = 0; j < 8; j++) {
+    for (int q = 0; q < C; q++) {
+      const CI<T> th = th1[j * C + q];  // shared memory, uniform: a broadcast
       const int idx = t + 512 * j + 4096 * q;
       const T x = idx < n ? digit_val<T>((unsigned)dig[idx]) : T(0);
       v[j].rl = DR<T>::fma_rd(x, th.rl, v[j].rl);
@@ -269,20 +278,9 @@ __device__ __forceinline__ void cross_pass1(const uint8_t *__restrict__ dig, int
       v[j].il = DR<T>::fma_rd(x, th.il, v[j].il);
       v[j].ih = DR<T>::fma_ru(x, th.ih, v[j].ih);
     }
-  }
-  if (crank & 1u) {
-#pragma unroll
-    for (int j = 0; j < 8; j++) {
-      const T il = v[j].il;
-      v[j].il = TB<T>::neg(v[j].ih);
-      v[j].ih = TB<T>::neg(il);
-    }
-  }
-  // local pass 1: row k0 = 0, twiddle of input q at pp.tw + (q - 1) (angles < pi/2 for q <= 4)
-#pragma unroll
-  for (int q = 1; q < 8; q++) {
-    const TwC<T> w = twb[pp.tw + q - 1];
-    v[q] = (2 * q <= 8) ? rtmul<T, false, false>(w, v[q]) : rtmul<T, false, true>(w, v[q]);
+    // (keeps the next input's loads after this one's FMAs: hoisting them all
+    // would cost registers the DFT needs)
+    asm volatile("" ::: "memory");
   }
   cdft<T, 8, false>(v);
 }
@@ -338,11 +336,12 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
   }
   __syncthreads();
   if (threadIdx.x == 0 && cid < kp.batch) {
-    mbar_expect(&tbar, EB * (X::FLAST + X::MF_ENT + X::MI_ENT + 2 * C));
+    mbar_expect(&tbar, EB * (X::FLAST + X::MF_ENT + X::MI_ENT + 2 * C + 16 * C));
     bulk_copy(twb + X::S_SWAP, tw + X::FWD(crank) + X::FP(4), EB * X::FLAST, &tbar);
     bulk_copy(twb + X::S_MF, tw + X::FWD(crank), EB * X::MF_ENT, &tbar);
     bulk_copy(twb + X::S_MI, tw + X::INV, EB * X::MI_ENT, &tbar);
     bulk_copy(twb + X::S_TH, tw + X::TH(crank), EB * 2 * C, &tbar);
+    bulk_copy(twb + X::S_TH1, tw + X::TH1(crank), EB * 16 * C, &tbar);
     if (staged) {  // operand a of the first pair (dbar phases: a = even, b = odd)
       mbar_expect(&dbar, (unsigned)n);
       bulk_copy(sdig, kp.a + (size_t)cid * n, (unsigned)n, &dbar);
@@ -370,7 +369,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
       if (staged) {  // the cross pass fused with local pass 1, stored in the pass-2 layout
         const PassRT pp = pick_fwd4<M>(0);
         CI<T> v[R];
-        cross_pass1<T, M>(sdig, n, theta, crank, twb, pp, v);
+        cross_pass1<T, M>(sdig, n, reinterpret_cast<const CI<T> *>(twb + X::S_TH1), v);
         if (op == 0 && it > 0) cluster_wait();  // the previous pair's remote reads of this state are done
         const int nu = (int)threadIdx.x;
 #pragma unroll
@@ -435,7 +434,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
           for (int r = 0; r < R; r++) {
             const CI<T> a = an;
             if (r + 1 < R) an = A.ld((r + 1) * (pp.L >> 1) + k0);
-            v[r] = cmul_ss(a, v[r]);
+            v[r] = cmul_ss<T, true>(a, v[r]);
           }
           cdft<T, R, true>(v);
           __syncthreads();

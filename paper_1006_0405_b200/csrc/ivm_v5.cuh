@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
           for (int r = 0; r < R; r++) {
             const CI<T> a = an;
             if (r + 1 < R) an = A.ld((r + 1) * (pp.L >> 1) + k0);
-            v[r] = cmul_ss(a, v[r]);
+            v[r] = cmul_ss<T, true>(a, v[r]);
           }
           cdft<T, R, true>(v);
           __syncthreads();
