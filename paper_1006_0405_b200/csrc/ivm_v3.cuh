@@ -467,12 +467,14 @@ struct CertAcc {  // per-thread; reduced once per multiplication
 // destinations are used only for n <= 32768 (m <= 2^16), where every certified
 // coefficient is an exact convolution value <= 255^2 n < 2^31; m = 2^17, 2^18
 // use int64 destinations (v5)
-template <typename T, typename D>
+// (DUMP = false: the caller has no interval dump; callers branch once on the dump
+// pointer around a whole emit loop, so the common path carries no dump code)
+template <typename T, typename D, bool DUMP = true>
 __device__ __forceinline__ void certify_real(T lo, T hi, int i, int n, D *dst, CertAcc &acc, double *dump) {
   // the odd-frequency kernels compute each coefficient as a REAL containment
   // interval (R13): the imaginary slots of the dump are NaN ("not
   // computed"), never a synthetic [0, 0]
-  if (dump) {
+  if (DUMP && dump) {
     const double qnan = __longlong_as_double(0x7ff8000000000000LL);
     reinterpret_cast<double4 *>(dump)[i] = make_double4((double)lo, (double)hi, qnan, qnan);
   }
@@ -541,14 +543,14 @@ __device__ __forceinline__ void emit_coeffs(const CI<T> &o, int k, const TwC<T> 
 // folded variant: the input twiddles already carried z^{-k0}; the remaining
 // factor z^{-L r} = conj(w_RATIO^r) (RATIO = 2m/L) is a compile-time constant
 // (c_k -> *d0, c_{k+m/2} -> *d1)
-template <typename T, int M, int RATIO>
+template <typename T, int M, int RATIO, bool DUMP = true>
 __device__ __forceinline__ void emit_fold(const CI<T> &o, int r, int k, int n, int32_t *d0, int32_t *d1,
                                           CertAcc &acc, double *dump) {
   constexpr int N = 1 << M;
   const CI<T> v = ctw<T, true>(o, r, RATIO);  // (the input twiddles carried the scale 2/m)
-  certify_real(v.rl, v.rh, k, n, d0, acc, dump);
-  certify_real(v.il, v.ih, k + N / 2, n, d1, acc, dump);
-  dump_prerot(dump, k, N, o, T(1));
+  certify_real<T, int32_t, DUMP>(v.rl, v.rh, k, n, d0, acc, dump);
+  certify_real<T, int32_t, DUMP>(v.il, v.ih, k + N / 2, n, d1, acc, dump);
+  if (DUMP) dump_prerot(dump, k, N, o, T(1));
 }
 
 template <typename T, int M, int RK, bool WARP = false, int QS = 0>
@@ -872,10 +874,19 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
         invR<T, R, true>(st, twb, pp, v, k0, nu);
         __syncthreads();  // every input loaded: the coefficients may overwrite the state
         double *dump = diag_dump(kp, pair, N);
+        if (dump) {
 #pragma unroll
-        for (int r = 0; r < R; r++) {
-          const int k = k0 + pp.L * r;
-          emit_fold<T, M, RATIO>(v[r], r, k, n, coef + cpos<QS>(k), coef + cpos<QS>(k + N / 2), acc, dump);
+          for (int r = 0; r < R; r++) {
+            const int k = k0 + pp.L * r;
+            emit_fold<T, M, RATIO, true>(v[r], r, k, n, coef + cpos<QS>(k), coef + cpos<QS>(k + N / 2), acc, dump);
+          }
+        } else {
+#pragma unroll
+          for (int r = 0; r < R; r++) {
+            const int k = k0 + pp.L * r;
+            emit_fold<T, M, RATIO, false>(v[r], r, k, n, coef + cpos<QS>(k), coef + cpos<QS>(k + N / 2), acc,
+                                          nullptr);
+          }
         }
       } else {
         invR<T, R, false>(st, twb, pp, v, k0, nu);

@@ -503,13 +503,24 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
       __syncthreads();  // every twiddle read: the swap buffer takes the coefficients
       IVM_PH(13);
       double *dump = diag_dump(kp, pair, N);
+      if (dump) {
 #pragma unroll
-      for (int g = 0; g < G; g++) {
-        const int kl = (int)threadIdx.x + 512 * g, k0 = (int)crank * B + kl;
+        for (int g = 0; g < G; g++) {
+          const int kl = (int)threadIdx.x + 512 * g, k0 = (int)crank * B + kl;
 #pragma unroll
-        for (int r = 0; r < C; r++)
-          emit_fold<T, M, 4 * C>(v[g][r], r, k0 + 4096 * r, n, coefL + r * B + cpos<B / 16>(kl),
-                                 coefL + (C + r) * B + cpos<B / 16>(kl), acc, dump);
+          for (int r = 0; r < C; r++)
+            emit_fold<T, M, 4 * C, true>(v[g][r], r, k0 + 4096 * r, n, coefL + r * B + cpos<B / 16>(kl),
+                                         coefL + (C + r) * B + cpos<B / 16>(kl), acc, dump);
+        }
+      } else {
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+          const int kl = (int)threadIdx.x + 512 * g, k0 = (int)crank * B + kl;
+#pragma unroll
+          for (int r = 0; r < C; r++)
+            emit_fold<T, M, 4 * C, false>(v[g][r], r, k0 + 4096 * r, n, coefL + r * B + cpos<B / 16>(kl),
+                                          coefL + (C + r) * B + cpos<B / 16>(kl), acc, nullptr);
+        }
       }
     }
     cert_flush(acc, cs);
