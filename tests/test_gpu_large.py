@@ -163,3 +163,45 @@ def test_cluster_and_group_corun(n, monkeypatch):
     assert np.array_equal(res["0"]["cert"], res["1"]["cert"])
     o = oracle.ivmul(a[[B - 1]], b[[B - 1]])
     assert res["1"]["max_radius"][B - 1] <= 2 * o["max_radius"][0]
+
+
+@pytest.mark.parametrize("n", [40001, 65537])
+def test_group_kernel_odd_n_byte_loads(ctx, n):
+    """n % 4 != 0 at m = 2^17 / 2^18: the tensor-core cross pass (DESIGN R16)
+    assembles its digit words from byte loads instead of word loads; products,
+    coefficients, containment, flags and radii against the oracle."""
+    kinds = np.array([0, 1, 2])
+    a, b = inputs.pair_digits(0x0DD1 + n, np.arange(3), n, kinds)
+    check_pairs(ctx, a, b, dump_n=2, oracle_sample=[0, 1])
+
+
+@pytest.mark.parametrize("n", [40000, 75000])
+def test_group_kernel_misaligned_operands(ctx, n):
+    """Operands at odd byte offsets at m = 2^17 / 2^18 (the cross pass's word
+    loads need 4-byte aligned rows; it falls back to byte loads): identical,
+    exact products."""
+    import torch
+    B = 3
+    a, b = inputs.pair_digits(0x0DD2 + n, np.arange(B), n, np.array([0, 1, 3]))
+    ta = torch.zeros(B * n + 1, dtype=torch.uint8, device="cuda")
+    tb = torch.zeros(B * n + 2, dtype=torch.uint8, device="cuda")
+    ta[1:] = torch.from_numpy(a.reshape(-1)).cuda()
+    tb[2:] = torch.from_numpy(b.reshape(-1)).cuda()
+    out, cert = ctx.multiply(ta[1:].view(B, n), tb[2:].view(B, n))
+    torch.cuda.synchronize()
+    assert cert.cpu().numpy().all()
+    o = out.cpu().numpy()
+    for p in range(B):
+        assert to_int(o[p]) == to_int(a[p]) * to_int(b[p]), p
+
+
+def test_config_C3_radius_tightness(ctx):
+    """The exact tensor-core cross pass (DESIGN R16) keeps C3's enclosures well
+    inside the north-star bar: GPU max radius <= 0.75 x the oracle's on a
+    uniform and an all-255 pair (round 1, FP64 direct sums: up to 0.56)."""
+    a, b, kinds = inputs.config_inputs("C3")
+    sel = [0, 32]
+    g = gpu_run(ctx, a[sel], b[sel])
+    r = oracle.ivmul(a[sel], b[sel])
+    assert g["cert"].all() and r["cert"].all()
+    assert np.all(g["max_radius"] <= 0.75 * r["max_radius"]), (g["max_radius"], r["max_radius"])
