@@ -823,7 +823,7 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
         bulk_copy(sdig + n, kp.b + (size_t)nxt * n, n, &dbar);
       }
       IVM_PH(2 * op);
-#pragma unroll 1
+#pragma unroll  // (specialised per pass: addresses fold into immediates)
       for (int i = 0; i < NFWD; i++) {
         const PassRT pp = pick_fwd<M, R>(i);
         CI<T> v[R];
@@ -864,7 +864,7 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
     }
     CertAcc acc;
     acc.radius = kp.max_radius != nullptr;
-#pragma unroll 1
+#pragma unroll  // (specialised per pass: addresses fold into immediates)
     for (int i = 0; i < NINV; i++) {
       const PassRT pp = pick_inv<M, R>(i);
       CI<T> v[R];

@@ -426,22 +426,20 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
           emit_tab<T, M>(v[g][r], fold[2 * r], k0 + 4096 * r, n, coefL + r * B + cpos<B / 16>(kl), coefL + (C + r) * B + cpos<B / 16>(kl), acc, dump);
       }
     } else {
-      // gather + input twiddles: y_q(kl) -> state[q B + kl]
-#pragma unroll
-      for (int j = 0; j < 8; j++) {
-        const int idx = (int)threadIdx.x + 512 * j, q = idx / B, kl = idx % B;
-        const int src = (2 * q < C) ? 2 * q : 2 * C - 1 - 2 * q;
-        CI<T> z = ldcg_ci(xch + (size_t)src * 4096 + (int)crank * B + kl);
-        const TwC<T> w = twb[X::S_SWAP + q * B + kl];
-        z = (2 * q < C) ? rtmul<T, true, true>(w, z) : rtmul_cd<T, false, true>(w, z);
-        st.st(idx, z);
-      }
-      __syncthreads();
-      {  // stage 1: task (b, kl), DFT8 over a, times w_C^{-b r1}
+      {  // stage 1: task (b, kl): its inputs y_q(kl), q = C2 a + b, gathered straight from
+         // the exchange (L2, coalesced over kl) with their input twiddles; DFT8 over a,
+         // times w_C^{-b r1}.  The state is free (every local pass finished before the
+         // group barrier), so the outputs are stored without a barrier.
         const int b = (int)threadIdx.x / B, kl = (int)threadIdx.x % B;
         CI<T> v[8];
 #pragma unroll
-        for (int a = 0; a < 8; a++) v[a] = st.ld((C2 * a + b) * B + kl);
+        for (int a = 0; a < 8; a++) {
+          const int q = C2 * a + b;
+          const int src = (2 * q < C) ? 2 * q : 2 * C - 1 - 2 * q;
+          const CI<T> z = ldcg_ci(xch + (size_t)src * 4096 + (int)crank * B + kl);
+          const TwC<T> w = twb[X::S_SWAP + q * B + kl];
+          v[a] = (2 * q < C) ? rtmul<T, true, true>(w, z) : rtmul_cd<T, false, true>(w, z);
+        }
         cdft<T, 8, true>(v);
 #pragma unroll
         for (int r1 = 1; r1 < 8; r1++) {  // b is warp-uniform (B >= 32)
@@ -449,7 +447,6 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
           const TwC<T> w = s2tw[2 * j];
           v[r1] = 2 * j <= C ? rtmul<T, true, true>(w, v[r1]) : rtmul<T, false, true>(w, v[r1]);
         }
-        __syncthreads();
 #pragma unroll
         for (int r1 = 0; r1 < 8; r1++) st.st((r1 * C2 + b) * B + kl, v[r1]);
         __syncthreads();
