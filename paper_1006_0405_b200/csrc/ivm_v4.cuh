@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
           bulk_copy(sdig, nx, (unsigned)n, &dbar);
         }
       }
-#pragma unroll 1
+#pragma unroll  // (specialised per pass: addresses fold into immediates)
       for (int i = 1; i < 4; i++) {
         const PassRT pp = pick_fwd4<M>(i);
         CI<T> v[R];
@@ -450,7 +450,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
       IVM_PH(2 * op + 1);
     }
     CertAcc acc;
-#pragma unroll 1
+#pragma unroll  // (specialised per pass: addresses fold into immediates)
     for (int i = 0; i < 3; i++) {
       const PassRT pp = pick_inv4<M>(i);
       CI<T> v[R];

@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
       }
       __syncthreads();
       IVM_PH(2 * op);
-#pragma unroll 1
+#pragma unroll  // (specialised per pass: addresses fold into immediates)
       for (int i = 0; i < 4; i++) {
         const PassRT pp = pick_fwd4<M>(i);
         CI<T> v[R];
@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v5_kernel(KParams kp, Group5 g) {
       }
       IVM_PH(2 * op + 1);
     }
-#pragma unroll 1
+#pragma unroll  // (specialised per pass: addresses fold into immediates)
     for (int i = 0; i < 3; i++) {
       const PassRT pp = pick_inv4<M>(i);
       CI<T> v[R];
