@@ -632,10 +632,21 @@ __device__ __forceinline__ PassRT pick_inv(int i) {
   return i == 0 ? p0 : (i == 1 ? p1 : p2);
 }
 
+// split write-after-read barrier of an in-place pass:
+// each warp's lane 0 arrives on `bar` (count = warps) once the warp's state loads
+// are done (__syncwarp orders the lanes' loads before lane 0's release-arrive)
+__device__ __forceinline__ void pb_arrive_warp(unsigned long long *bar) {
+  __syncwarp();
+  if ((threadIdx.x & 31u) == 0u) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+  }
+}
+
 // forward: F_p[k0][nu + Sp q] * w_{2LR}^{q(2k0+1)} -> R-point DFT
 template <typename T, int R>
 __device__ __forceinline__ void fwdR(Buf<T> st, const TwC<T> *twb, const PassRT &pp, CI<T> (&v)[R], int &k0,
-                                     int &nu, int t = threadIdx.x) {
+                                     int &nu, int t = threadIdx.x, unsigned long long *wbar = nullptr) {
   const int Sp = 1 << pp.lgSp;
   k0 = t >> pp.lgSp;
   nu = t & (Sp - 1);
@@ -651,13 +662,14 @@ __device__ __forceinline__ void fwdR(Buf<T> st, const TwC<T> *twb, const PassRT 
     }
     v[q] = z;
   }
+  if (wbar) pb_arrive_warp(wbar);
   cdft<T, R, false>(v);
 }
 
 // inverse: E_p[k0][mu] (mirror for q >= R/2) * twiddle -> R-point inverse DFT
 template <typename T, int R, bool FOLD>
 __device__ __forceinline__ void invR(Buf<T> st, const TwC<T> *twb, const PassRT &pp, CI<T> (&v)[R], int &k0,
-                                     int &nu, int t = threadIdx.x) {
+                                     int &nu, int t = threadIdx.x, unsigned long long *wbar = nullptr) {
   const int Sp = 1 << pp.lgSp, lgH = pp.lgSp - 1, S = R * Sp;
   k0 = t >> lgH;
   nu = t & ((Sp >> 1) - 1);
@@ -683,6 +695,7 @@ __device__ __forceinline__ void invR(Buf<T> st, const TwC<T> *twb, const PassRT 
     }
     v[q] = z;
   }
+  if (wbar) pb_arrive_warp(wbar);
   cdft<T, R, true>(v);
 }
 
@@ -755,9 +768,15 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
   constexpr int N = C::N;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Cert3 cs;
-  __shared__ __align__(8) unsigned long long tbar, dbar;
+  __shared__ __align__(8) unsigned long long tbar, dbar, pbar;
   Buf<T> st{reinterpret_cast<V *>(smem), reinterpret_cast<V *>(smem) + C::CAP};
   int32_t *coef = reinterpret_cast<int32_t *>(smem);  // aliases the state (see Cfg3)
+#ifdef IVM_NO_SPLITBAR
+  unsigned long long *wbar = nullptr;
+#else
+  unsigned long long *wbar = &pbar;  // split write-after-read barrier of the mid passes
+#endif
+  unsigned pph = 0u;
   TwC<T> *twb = reinterpret_cast<TwC<T> *>(smem + C::STATE_BYTES);
   uint8_t *sdig = smem + C::STATE_BYTES + C::TW_BYTES;
   Buf<T> A{reinterpret_cast<V *>(kp.ascratch) + (size_t)blockIdx.x * N, nullptr};
@@ -779,6 +798,8 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
   if (threadIdx.x == 0) {
     mbar_init(&tbar);
     mbar_init(&dbar);
+    const unsigned a = (unsigned)__cvta_generic_to_shared(&pbar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"((unsigned)(C::THREADS / 32)));
   }
   __syncthreads();
   if (threadIdx.x == 0 && blockIdx.x < kp.batch) {
@@ -829,9 +850,14 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
         CI<T> v[R];
         int k0, nu;
         if (LAST16 && op == 0 && pp.big) mbar_wait(&tbar, 0);  // forward-last table restored
-        fwdR<T, R>(st, twb, pp, v, k0, nu);
+        fwdR<T, R>(st, twb, pp, v, k0, nu, threadIdx.x, i < NFWD - 1 ? wbar : nullptr);
         if (i < NFWD - 1) {  // mid pass: store both halves (mirror conjugated)
-          __syncthreads();
+          if (wbar) {
+            mbar_wait(wbar, pph);
+            pph ^= 1u;
+          } else {
+            __syncthreads();
+          }
 #pragma unroll
           for (int r = 0; r < R; r++) {
             if (2 * r < R) st.st(sidx(k0 + pp.L * r, nu, pp.RSo, pp.SWo), v[r]);
@@ -889,8 +915,13 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
           }
         }
       } else {
-        invR<T, R, false>(st, twb, pp, v, k0, nu);
-        __syncthreads();
+        invR<T, R, false>(st, twb, pp, v, k0, nu, threadIdx.x, wbar);
+        if (wbar) {
+          mbar_wait(wbar, pph);
+          pph ^= 1u;
+        } else {
+          __syncthreads();
+        }
 #pragma unroll
         for (int r = 0; r < R; r++) st.st(sidx(k0 + pp.L * r, nu, pp.RSo, pp.SWo), v[r]);
       }
