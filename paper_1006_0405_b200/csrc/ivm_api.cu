@@ -28,6 +28,9 @@ struct ivm_ctx {
   std::map<std::pair<int, int>, ivm::LaunchInfo> info3;
   bool force_v1 = false;
   bool force_v5 = false;   // IVM_KERNEL=v5: the group kernel also for m = 2^14 .. 2^16
+  bool v7 = true;          // fp64 m = 2^17, 2^18: the pipelined group kernel (IVM_V7=0: the lockstep one)
+  void *g7scratch = nullptr;  // its stage counters and per-pair ring
+  size_t g7scratch_bytes = 0;
   std::map<std::pair<int, int>, void *> tw4;  // (log2m, prec) -> v4 role tables
   std::map<std::pair<int, int>, ivm::LaunchInfo> info4;
   std::map<std::pair<int, int>, void *> twn;  // (log2m, prec) -> round-to-nearest twiddles (naive SS)
@@ -179,6 +182,10 @@ int ivm_create(ivm_ctx_t *ctx, int device) {
   const char *kv = getenv("IVM_KERNEL");
   c->force_v1 = kv && strcmp(kv, "v1") == 0;
   c->force_v5 = kv && strcmp(kv, "v5") == 0;
+  {
+    const char *e = getenv("IVM_V7");
+    c->v7 = !(e && strcmp(e, "0") == 0);
+  }
   {  // IVM_CORUN=0 disables the co-run; IVM_CORUN_EFF sets the group kernel's relative rate
     const char *e = getenv("IVM_CORUN");
     c->corun = !(e && strcmp(e, "0") == 0);
@@ -210,6 +217,7 @@ int ivm_destroy(ivm_ctx_t c) {
   cudaFree(c->slot);
   cudaFree(c->stage);
   cudaFree(c->gscratch);
+  cudaFree(c->g7scratch);
   cudaFree(c->lscratch);
   if (c->s_in) cudaStreamDestroy(c->s_in);
   if (c->s_out) cudaStreamDestroy(c->s_out);
@@ -249,6 +257,7 @@ static bool use_v3(ivm_ctx_t c, int m) { return !c->force_v1 && m >= 10 && m <= 
 static bool use_v6(ivm_ctx_t c, int m, int prec) { return !c->force_v1 && prec == IVM_F64 && m >= 6 && m <= 9; }
 static bool use_v4(ivm_ctx_t c, int m) { return !c->force_v5 && m >= 14 && m <= 16; }
 static bool use_v5(ivm_ctx_t c, int m) { return m >= 14 && m <= 18 && !use_v4(c, m); }
+static bool use_v7(ivm_ctx_t c, int m, int prec) { return c->v7 && prec == IVM_F64 && (m == 17 || m == 18); }
 
 static int get_info5(ivm_ctx_t c, int m, int prec, ivm::LaunchInfo *li) {
   auto key = std::make_pair(m + 100, prec);
@@ -258,6 +267,20 @@ static int get_info5(ivm_ctx_t c, int m, int prec, ivm::LaunchInfo *li) {
     return IVM_OK;
   }
   int r = ivm::v5_info(prec, m, li);
+  if (r == -4) return IVM_EUNSUPPORTED;
+  if (r != 0 || li->blocks_per_sm < 1) return cuda_fail(c);
+  c->info4[key] = *li;
+  return IVM_OK;
+}
+
+static int get_info7(ivm_ctx_t c, int m, ivm::LaunchInfo *li) {
+  auto key = std::make_pair(m + 200, (int)IVM_F64);
+  auto it = c->info4.find(key);
+  if (it != c->info4.end()) {
+    *li = it->second;
+    return IVM_OK;
+  }
+  int r = ivm::v7_info(m, li);
   if (r == -4) return IVM_EUNSUPPORTED;
   if (r != 0 || li->blocks_per_sm < 1) return cuda_fail(c);
   c->info4[key] = *li;
@@ -410,6 +433,55 @@ static int launch_v5(ivm_ctx_t c, int m, int prec, const ivm::KParams &kp0, size
   return IVM_OK;
 }
 
+// The pipelined group kernel (v7): grid, ring size and scratch.  A pair's tasks
+// span at most two consecutive slots, its last stage runs three slots after its
+// first task's; the L stage of pair p + rp waits for pair p's last stage, which
+// must lie at an earlier slot: rp C >= 5 grid + C - 1 (ivm_v7.cuh)
+static int ensure_scratch(ivm_ctx_t c, size_t bytes);
+static int v7_ring(size_t grid, size_t C, size_t batch, size_t pair_bytes) {
+  size_t rp = (5 * grid + C - 1) / C + 1;
+  // a larger ring when memory allows (up to 1 GB): no slot reuse, so no ring waits, below 1 GB
+  const size_t cap = ((size_t)1 << 30) / pair_bytes;
+  if (cap > rp) rp = cap;
+  if (rp > batch) rp = batch;
+  return (int)rp;
+}
+static int launch_v7(ivm_ctx_t c, int m, const ivm::KParams &kp0, const ivm::LaunchInfo &li, size_t batch,
+                     cudaStream_t s) {
+  const size_t C = (size_t)li.cluster;
+  size_t grid = (size_t)c->sms * li.blocks_per_sm;
+  if (grid > batch * C) grid = batch * C;
+  const size_t per_pair = C * 4096 * 32 + C * 512 * 16 + 2 * C * C * 8 + C * 32;
+  const size_t rp = (size_t)v7_ring(grid, C, batch, per_pair);
+  const size_t al = 256;
+  auto up = [&](size_t x) { return (x + al - 1) / al * al; };
+  const size_t b_cnt = up(batch * 16), b_x = up(rp * C * 4096 * 32), b_w = up(rp * C * 512 * 16),
+               b_r = up(rp * 2 * C * C * 8), b_l = up(rp * C * 32);
+  const size_t need = b_cnt + b_x + b_w + b_r + b_l;
+  int r = ensure_scratch(c, grid * li.a_bytes_per_cta);
+  if (r) return r;
+  if (c->g7scratch_bytes < need) {
+    cudaFree(c->g7scratch);
+    c->g7scratch = nullptr;
+    c->g7scratch_bytes = 0;
+    if (cudaMalloc(&c->g7scratch, need) != cudaSuccess) return IVM_ENOMEM;
+    c->g7scratch_bytes = need;
+  }
+  char *gs = (char *)c->g7scratch;
+  ivm::Pipe7Args pa;
+  pa.cnt = (unsigned *)gs;
+  pa.xch = gs + b_cnt;
+  pa.wds = (uint4 *)(gs + b_cnt + b_x);
+  pa.rec = (uint2 *)(gs + b_cnt + b_x + b_w);
+  pa.link = (unsigned *)(gs + b_cnt + b_x + b_w + b_r);
+  pa.rp = (int)rp;
+  if (cudaMemsetAsync(pa.cnt, 0, b_cnt, s) != cudaSuccess) return cuda_fail(c);
+  ivm::KParams kp = kp0;
+  kp.ascratch = c->ascratch;
+  if (ivm::v7_launch(m, kp, pa, (int)grid, s) != 0) return cuda_fail(c);
+  return IVM_OK;
+}
+
 // Co-run split of a cluster-kernel batch (m = 2^14 .. 2^16): clusters of C CTAs
 // must sit inside one GPC, so `cl` clusters strand sms - cl C SMs; `g5` groups
 // of the group kernel (same C, exchange through L2) run there at a per-group
@@ -481,6 +553,13 @@ int ivm_reserve(ivm_ctx_t c, size_t n, size_t batch, int prec) {
     size_t grid = (batch + li.cluster - 1) / li.cluster, cap = (size_t)c->sms * li.blocks_per_sm;
     if (grid > cap) grid = cap;
     return ensure_scratch(c, grid * li.a_bytes_per_cta);
+  }
+  if (use_v7(c, m, prec)) {
+    const void *t4;
+    ivm::LaunchInfo li;
+    int r = get_table4(c, m, prec, &t4);
+    if (!r) r = get_info7(c, m, &li);
+    return r;
   }
   if (use_v5(c, m)) {
     const void *t4;
@@ -610,6 +689,18 @@ int ivm_multiply_batched_diag(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, s
     kp.ascratch = c->ascratch;
     kp.tw = tw;
     if (ivm::v6_launch(prec, m, kp, (int)grid, s) != 0) return cuda_fail(c);
+    c->last_launches = launches + 1;
+    return IVM_OK;
+  }
+  if (use_v7(c, m, prec)) {
+    const void *tw;
+    ivm::LaunchInfo li;
+    r = get_table4(c, m, prec, &tw);
+    if (!r) r = get_info7(c, m, &li);
+    if (r) return r;
+    kp.tw = tw;
+    r = launch_v7(c, m, kp, li, batch, s);
+    if (r) return r;
     c->last_launches = launches + 1;
     return IVM_OK;
   }

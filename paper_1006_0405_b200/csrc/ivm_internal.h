@@ -66,6 +66,19 @@ struct Group5Args {
 int upload_w64_v5(const double *w64, const float *w32);
 int v5_info(int prec, int m, LaunchInfo *li);
 int v5_launch(int prec, int m, const KParams &kp, const Group5Args &ga, int groups, cudaStream_t s, bool coop);
+// m = 2^17, 2^18, fp64: the pipelined group kernel (ivm_v7.cuh): a persistent
+// grid of one CTA per SM dealing the batch's batch x C tasks; per-pair scratch in
+// a ring of rp pairs (v7_ring)
+struct Pipe7Args {
+  unsigned *cnt;     // [batch][4], zeroed before every launch
+  void *xch;         // [rp][C][4096] complex intervals
+  uint4 *wds;        // [rp][C][512]
+  uint2 *rec;        // [rp][2 C^2]
+  unsigned *link;    // [rp][C][8]
+  int rp;
+};
+int v7_info(int m, LaunchInfo *li);
+int v7_launch(int m, const KParams &kp, const Pipe7Args &pa, int grid, cudaStream_t s);
 
 // batch summary {certified count, max radius} into out[2] (device), zeroed first
 int summary_launch(const uint8_t *cert, const double *rad, int batch, double *out, cudaStream_t s);

@@ -31,8 +31,11 @@ NAMES = {
     "v5": ["cross a", "passes a", "cross b", "passes b + pointwise + inv0", "inverse local passes + xch",
            "group barrier 1", "last pass (L2) + emit", "boundary + group barrier 2", "cert + prev fetch",
            "carry scan", "group barrier 3", "carry emit + tail"],
+    "v7": ["L: cross a", "L: passes a", "L: cross b", "L: passes b + pointwise + inv0",
+           "L: inverse local passes + xch", "A: wait", "A: last pass (L2) + emit", "A: chunk carry + publish",
+           "Cs: wait", "Cs: resolve + digits", "(unused)", "(unused)", "L: ring wait"],
 }
-KERNEL = {"C1": "v3", "C2": "v3", "C3": "v5", "C5": "v4"}
+KERNEL = {"C1": "v3", "C2": "v3", "C3": "v7" if os.environ.get("IVM_V7", "1") != "0" else "v5", "C5": "v4"}
 
 
 def build():
