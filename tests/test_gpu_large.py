@@ -238,3 +238,35 @@ def test_pipelined_group_kernel_matches_lockstep(n, B, monkeypatch):
     okp = g["cert"].astype(bool)
     assert not g["prod"][~okp].any()
     assert oracle.residue_check(a[okp], b[okp], g["prod"][okp]).all()
+
+
+@pytest.mark.parametrize("n", [40000, 75000])
+def test_large_m_carry_patterns(ctx, n):
+    """Products whose digits run through long stretches of 0xFF and 0x00 across
+    chunk boundaries (the chunk carry: generate / propagate / a carry arriving
+    only through the value passed up from the chunk below): a = 256^n - 1 times
+    b in {1, 256^j + 1, 256^j - 1 (j = n / 3), 2, 255, 256^(n-1) + 1,
+    random digits in [0, 1]}, bit-exact against Python integers."""
+    import torch
+    B = 8
+    a = np.full((B, n), 255, np.uint8)
+    b = np.zeros((B, n), np.uint8)
+    j = n // 3
+    b[0, 0] = 1
+    b[1, 0] = 1
+    b[1, j] = 1
+    b[2, :j] = 255
+    b[3, 0] = 2
+    b[4, 0] = 255
+    b[5, 0] = 1
+    b[5, n - 1] = 1
+    rng = np.random.default_rng(n)
+    b[6] = rng.integers(0, 2, n, dtype=np.uint8)
+    a[7] = rng.integers(254, 256, n, dtype=np.uint8)
+    b[7] = 255
+    out, cert = ctx.multiply(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
+    torch.cuda.synchronize()
+    cert, out = cert.cpu().numpy(), out.cpu().numpy()
+    assert cert.all()
+    for p in range(B):
+        assert to_int(out[p]) == to_int(a[p]) * to_int(b[p]), p
