@@ -42,11 +42,13 @@ struct Pipe7 {
   int rp;           // ring pairs
 };
 
-// stage counters: the CTA's writes (ordered before thread 0 by the block barrier
-// the caller places) are released by thread 0's gpu-scope add; a wait acquires
-// the other CTAs' releases and a block barrier passes it on
+// stage counters: the CTA's writes (ordered before the posting thread by the block
+// barrier the caller places) are released by one thread's gpu-scope add -- the
+// last warp's, so that its wait for the stores to drain overlaps thread 0's poll
+// of the next stage's counter; a wait acquires the other CTAs' releases and a
+// block barrier passes it on
 __device__ __forceinline__ void post7(unsigned *c) {
-  if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(c) : "memory");
+  if (threadIdx.x == 480) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(c) : "memory");
 }
 __device__ __forceinline__ void await7(const unsigned *c, unsigned target) {
   if (threadIdx.x == 0) {
