@@ -117,6 +117,11 @@ static int v3_info_impl(LaunchInfo *li) {
   auto k = v3::ivm_v3_kernel<T, M, R>;
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) != cudaSuccess)
     return -1;
+  if constexpr (sizeof(T) == 8) {  // the throughput variant (v3_go)
+    if (cudaFuncSetAttribute(v3::ivm_v3_kernel<T, M, R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)C::SMEM) != cudaSuccess)
+      return -1;
+  }
   int nb = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, C::THREADS, C::SMEM) != cudaSuccess) return -1;
   li->blocks_per_sm = nb;
@@ -134,6 +139,16 @@ int v3_info(int prec, int m, int radix, LaunchInfo *li) { IVM_V3_DISPATCH(v3_inf
 
 template <typename T, int M, int R> static void v3_go(const KParams &kp, int grid, cudaStream_t s) {
   using C = v3::Cfg3<T, M, R>;
+  // fp64 with 16-byte aligned digit rows and no diagnostic outputs: the kernel
+  // compiled without the unstaged-digit and dump paths (same arithmetic)
+  if constexpr (sizeof(T) == 8) {
+    const bool aligned = kp.n % 16 == 0 &&
+                         ((reinterpret_cast<uintptr_t>(kp.a) | reinterpret_cast<uintptr_t>(kp.b)) % 16 == 0);
+    if (aligned && !kp.dump_slot && !kp.coeffs) {
+      v3::ivm_v3_kernel<T, M, R, true><<<grid, C::THREADS, C::SMEM, s>>>(kp);
+      return;
+    }
+  }
   v3::ivm_v3_kernel<T, M, R><<<grid, C::THREADS, C::SMEM, s>>>(kp);
 }
 template <int M> static int v3_launch_m(int prec, int radix, const KParams &kp, int grid, cudaStream_t s) {

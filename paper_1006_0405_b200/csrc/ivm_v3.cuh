@@ -760,7 +760,10 @@ __device__ __forceinline__ double *diag_dump(const KParams &kp, int pair, int N)
   return s >= 0 ? kp.intervals + (size_t)s * N * 4 : nullptr;
 }
 
-template <typename T, int M, int R>
+// FAST: the host guarantees staged digits (16-byte aligned rows) and no diagnostic
+// outputs (interval dump, snapped coefficients), so those paths and the values they
+// keep live across the pair loop are compiled out of the throughput kernel
+template <typename T, int M, int R, bool FAST = false>
 __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) ivm_v3_kernel(KParams kp) {
   using C = Cfg3<T, M, R>;
   using Gm = G3<M, R>;
@@ -794,7 +797,7 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
   constexpr int QS = C::THREADS;  // coefficient layout of the 4-words-per-thread carry (cpos)
   // digits staged by bulk copies when every row is 16-byte aligned
   const bool staged =
-      (n % 16 == 0) && ((reinterpret_cast<uintptr_t>(kp.a) | reinterpret_cast<uintptr_t>(kp.b)) % 16 == 0);
+      FAST || ((n % 16 == 0) && ((reinterpret_cast<uintptr_t>(kp.a) | reinterpret_cast<uintptr_t>(kp.b)) % 16 == 0));
   if (threadIdx.x == 0) {
     mbar_init(&tbar);
     mbar_init(&dbar);
@@ -899,8 +902,8 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
         mbar_wait(&tbar, 1);  // folded table
         invR<T, R, true>(st, twb, pp, v, k0, nu);
         __syncthreads();  // every input loaded: the coefficients may overwrite the state
-        double *dump = diag_dump(kp, pair, N);
-        if (dump) {
+        double *dump = FAST ? nullptr : diag_dump(kp, pair, N);
+        if (!FAST && dump) {
 #pragma unroll
           for (int r = 0; r < R; r++) {
             const int k = k0 + pp.L * r;
@@ -927,7 +930,7 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
       }
       __syncthreads();
     }
-    if constexpr (!LAST16) inv_last<T, M, R, false, QS>(st, tw, n, coef, acc, diag_dump(kp, pair, N));
+    if constexpr (!LAST16) inv_last<T, M, R, false, QS>(st, tw, n, coef, acc, FAST ? nullptr : diag_dump(kp, pair, N));
     IVM_PH(4);
     cert_flush(acc, cs);
     __syncthreads();
@@ -938,7 +941,7 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
     }
     const bool certified = cs.ok != 0;
     carry_store4<QS>(coef, n, kp.prod + (size_t)pair * 2 * n, certified);
-    if (kp.coeffs) {
+    if (!FAST && kp.coeffs) {
       int64_t *co = kp.coeffs + (size_t)pair * (2 * n - 1);
       for (int i = threadIdx.x; i < 2 * n - 1; i += blockDim.x) co[i] = certified ? coef[cpos<QS>(i)] : 0;
     }
