@@ -167,6 +167,11 @@ template <typename T, int M> static int v4_info_impl(LaunchInfo *li) {
   li->a_bytes_per_cta = CF::A_BYTES;
   li->cluster = C;
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM) != cudaSuccess) return -1;
+  if constexpr (sizeof(T) == 8) {  // the throughput variant (v4_go)
+    if (cudaFuncSetAttribute(v4::ivm_v4_kernel<T, M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)CF::SMEM) != cudaSuccess)
+      return -1;
+  }
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -204,6 +209,14 @@ template <typename T, int M> static int v4_go(const KParams &kp, int clusters, c
   cfg.stream = s;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  // fp64, no diagnostic outputs and (where digits are staged) 16-byte aligned rows:
+  // the kernel compiled without those paths (same arithmetic)
+  if constexpr (sizeof(T) == 8) {
+    const bool aligned = CF::DIG_BYTES == 0 || (kp.n % 16 == 0 && ((reinterpret_cast<uintptr_t>(kp.a) |
+                                                                    reinterpret_cast<uintptr_t>(kp.b)) % 16 == 0));
+    if (aligned && !kp.dump_slot && !kp.coeffs)
+      return cudaLaunchKernelEx(&cfg, v4::ivm_v4_kernel<T, M, true>, kp) == cudaSuccess ? 0 : -1;
+  }
   return cudaLaunchKernelEx(&cfg, v4::ivm_v4_kernel<T, M>, kp) == cudaSuccess ? 0 : -1;
 }
 template <int M> static int v4_launch_m(int prec, const KParams &kp, int clusters, cudaStream_t s) {

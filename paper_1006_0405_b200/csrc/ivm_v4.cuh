@@ -300,7 +300,10 @@ template <typename T, int M> struct Cfg4 {
   static_assert(SMEM <= 227 * 1024, "shared memory");
 };
 
-template <typename T, int M>
+// FAST: the host guarantees no diagnostic outputs (interval dump, snapped
+// coefficients) and, where the digits are staged at all (m <= 2^15), 16-byte
+// aligned rows: the other paths are compiled out of the throughput kernel
+template <typename T, int M, bool FAST = false>
 __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
   using X = G4<M>;
   using GL = G3<13, 8>;
@@ -328,8 +331,9 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
   constexpr int RSI1 = GL::iRS(1), SWI1 = GL::iSW(1);
   constexpr unsigned EB = sizeof(TwC<T>);
 
-  const bool staged = CF::DIG_BYTES > 0 && n % 16 == 0 &&
-                      ((reinterpret_cast<uintptr_t>(kp.a) | reinterpret_cast<uintptr_t>(kp.b)) % 16) == 0;
+  const bool staged = CF::DIG_BYTES > 0 &&
+                      (FAST || (n % 16 == 0 &&
+                                ((reinterpret_cast<uintptr_t>(kp.a) | reinterpret_cast<uintptr_t>(kp.b)) % 16) == 0));
   if (threadIdx.x == 0) {
     mbar_init(&tbar);
     mbar_init(&dbar);
@@ -502,8 +506,8 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
       }
       __syncthreads();  // every twiddle read: the swap buffer takes the coefficients
       IVM_PH(13);
-      double *dump = diag_dump(kp, pair, N);
-      if (dump) {
+      double *dump = FAST ? nullptr : diag_dump(kp, pair, N);
+      if (!FAST && dump) {
 #pragma unroll
         for (int g = 0; g < G; g++) {
           const int kl = (int)threadIdx.x + 512 * g, k0 = (int)crank * B + kl;
@@ -638,7 +642,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
       for (int i = ch * B + 4 * tc; i < min(ch * B + B, nout); i += 4 * TPC)
         for (int b = 0; b < 4 && i + b < nout; b++) out[i + b] = 0;
     }
-    if (kp.coeffs) {
+    if (!FAST && kp.coeffs) {
       int64_t *co = kp.coeffs + (size_t)pair * nc;
       for (int l = tc; l < B && ch * B + l < nc; l += TPC) co[ch * B + l] = ok ? (int64_t)coefL[lc * B + cpos<TPC>(l)] : 0;
     }

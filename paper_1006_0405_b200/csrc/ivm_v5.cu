@@ -101,6 +101,9 @@ template <int M> static int v7_info_m(LaunchInfo *li) {
   li->a_bytes_per_cta = CF::A_BYTES;
   li->cluster = v4::G4<M>::C;
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM) != cudaSuccess) return -1;
+  if (cudaFuncSetAttribute(v7::ivm_v7_kernel<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM) !=
+      cudaSuccess)
+    return -1;
   int nb = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, CF::THREADS, CF::SMEM) != cudaSuccess) return -1;
   li->blocks_per_sm = nb;
@@ -119,8 +122,11 @@ template <int M> static int v7_go(const KParams &kp, const Pipe7Args &pa, int gr
   KParams k2 = kp;
   v7::Pipe7 g{pa.cnt, pa.xch, pa.wds, pa.rec, pa.link, pa.rp};
   void *args[] = {(void *)&k2, (void *)&g};
-  const cudaError_t e = cudaLaunchCooperativeKernel((const void *)v7::ivm_v7_kernel<M>, dim3(grid), dim3(CF::THREADS),
-                                                    args, CF::SMEM, s);
+  // word-aligned digit rows and no diagnostic outputs: the kernel compiled without those paths
+  const bool fast = kp.n % 4 == 0 && ((reinterpret_cast<uintptr_t>(kp.a) | reinterpret_cast<uintptr_t>(kp.b)) % 4 == 0) &&
+                    !kp.dump_slot && !kp.coeffs;
+  const void *fn = fast ? (const void *)v7::ivm_v7_kernel<M, true> : (const void *)v7::ivm_v7_kernel<M>;
+  const cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(CF::THREADS), args, CF::SMEM, s);
   return e == cudaSuccess ? 0 : -1;
 }
 int v7_launch(int m, const KParams &kp, const Pipe7Args &pa, int grid, cudaStream_t s) {

@@ -208,12 +208,13 @@ __device__ __forceinline__ void cross_tc_impl(const uint8_t *__restrict__ dig, i
   }
 }
 
-template <int M>
+// ALIGNED: the caller guarantees word-aligned rows (only the word-load body is compiled)
+template <int M, bool ALIGNED = false>
 __device__ __forceinline__ void cross_tc(const uint8_t *__restrict__ dig, int n, Buf<double> st, const void *limbs,
                                          unsigned crank) {
   unsigned bf[8];  // (reloaded per call: L1-resident, and no registers held across the passes)
   tc_limbs(limbs, crank, bf);
-  if (((reinterpret_cast<uintptr_t>(dig) | (uintptr_t)n) & 3) == 0) cross_tc_impl<M, true>(dig, n, st, bf, (crank & 1u) != 0u);
+  if (ALIGNED || ((reinterpret_cast<uintptr_t>(dig) | (uintptr_t)n) & 3) == 0) cross_tc_impl<M, true>(dig, n, st, bf, (crank & 1u) != 0u);
   else cross_tc_impl<M, false>(dig, n, st, bf, (crank & 1u) != 0u);
 }
 

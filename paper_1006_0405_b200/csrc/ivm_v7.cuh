@@ -60,7 +60,9 @@ __device__ __forceinline__ void await7(const unsigned *c, unsigned target) {
   __syncthreads();
 }
 
-template <int M>
+// FAST: the host guarantees word-aligned digit rows and no diagnostic outputs
+// (interval dump, snapped coefficients): those paths are compiled out
+template <int M, bool FAST = false>
 __global__ void __launch_bounds__(512, 1) ivm_v7_kernel(KParams kp, Pipe7 g) {
   using T = double;
   using X = G4<M>;
@@ -127,7 +129,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v7_kernel(KParams kp, Pipe7 g) {
       }
 #pragma unroll 1
       for (int op = 0; op < 2; op++) {
-        cross_tc<M>((op == 0 ? kp.a : kp.b) + (size_t)pair * n, n, st, tw + X::LIMB, role);
+        cross_tc<M, FAST>((op == 0 ? kp.a : kp.b) + (size_t)pair * n, n, st, tw + X::LIMB, role);
         __syncthreads();
         IVM_PH(2 * op);
 #pragma unroll  // (specialised per pass: addresses fold into immediates)
@@ -231,7 +233,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v7_kernel(KParams kp, Pipe7 g) {
       }
       {  // stage 2: task (r1, kl), DFT_C2 over b, untwist remainder, emit into the swap buffer
         constexpr int TASKS = 8 * B / 512;
-        double *dump = diag_dump(kp, pair, N);
+        double *dump = FAST ? nullptr : diag_dump(kp, pair, N);
 #pragma unroll
         for (int g2 = 0; g2 < TASKS; g2++) {
           const int task = (int)threadIdx.x + 512 * g2, r1 = task / B, kl = task % B;
@@ -288,7 +290,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v7_kernel(KParams kp, Pipe7 g) {
           g.rec[(size_t)slot * NCHT + ch] = make_uint2(hr, dout);
         }
         g.wds[((size_t)slot * C + role) * 512 + threadIdx.x] = make_uint4(U[0], U[1], U[2], U[3]);
-        if (kp.coeffs) {  // snapped coefficients (zeroed in the Cs stage if the pair fails)
+        if (!FAST && kp.coeffs) {  // snapped coefficients (zeroed in the Cs stage if the pair fails)
           int64_t *co = kp.coeffs + (size_t)pair * nc;
           for (int e = (int)threadIdx.x; e < NCH * B; e += blockDim.x) {
             const int lc2 = e / B, i = (lc2 * C + (int)role) * B + e % B;
@@ -432,7 +434,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v7_kernel(KParams kp, Pipe7 g) {
       } else {
         for (int i = ch * B + 4 * tc; i < min(ch * B + B, nout); i += 4 * TPC)
           for (int b = 0; b < 4 && i + b < nout; b++) out[i + b] = 0;
-        if (kp.coeffs) {
+        if (!FAST && kp.coeffs) {
           int64_t *co = kp.coeffs + (size_t)pair * nc;
           for (int e = (int)threadIdx.x; e < NCH * B; e += blockDim.x) {
             const int i = (e / B * C + (int)role) * B + e % B;
