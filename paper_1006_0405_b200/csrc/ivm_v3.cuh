@@ -643,6 +643,65 @@ __device__ __forceinline__ void pb_arrive_warp(unsigned long long *bar) {
   }
 }
 
+// radix-8 DIT of twiddled inputs, written so that the input twiddle products
+// (integer-heavy endpoint selects) of one half sit next to the butterflies
+// (FP64-dense) of the other in program order: in(q) gives input q times its
+// twiddle; operations and operands are exactly cdft<T, 8, INV>'s, so the result
+// is bit-identical -- only the instruction order the scheduler starts from changes
+template <typename T, bool INV, typename IN, typename AL>
+__device__ __forceinline__ void dit8(CI<T> (&v)[8], IN &&in, AL &&loaded) {
+  CI<T> a0 = in(0), a1 = in(4);
+  bfly(a0, a1, CI<T>(a1));
+  CI<T> a2 = in(2), a3 = in(6);
+  bfly(a2, a3, CI<T>(a3));
+  bfly(a0, a2, CI<T>(a2));
+  bfly(a1, a3, ctw<T, INV>(a3, 1, 4));
+  CI<T> a4 = in(1), a5 = in(5);
+  bfly(a4, a5, CI<T>(a5));
+  CI<T> a6 = in(3), a7 = in(7);
+  loaded();  // every input has been read
+  bfly(a6, a7, CI<T>(a7));
+  bfly(a4, a6, CI<T>(a6));
+  bfly(a5, a7, ctw<T, INV>(a7, 1, 4));
+  bfly(a0, a4, CI<T>(a4));
+  bfly(a1, a5, ctw<T, INV>(a5, 1, 8));
+  bfly(a2, a6, ctw<T, INV>(a6, 2, 8));
+  bfly(a3, a7, ctw<T, INV>(a7, 3, 8));
+  v[0] = a0, v[1] = a1, v[2] = a2, v[3] = a3, v[4] = a4, v[5] = a5, v[6] = a6, v[7] = a7;
+}
+
+// the input after q in dit8's order 0, 4, 2, 6, 1, 5, 3, 7 (-1: q was the last)
+__host__ __device__ constexpr int dit8_next(int q) {
+  return q == 0 ? 4 : q == 4 ? 2 : q == 2 ? 6 : q == 6 ? 1 : q == 1 ? 5 : q == 5 ? 3 : q == 3 ? 7 : -1;
+}
+
+// pointwise product with a's spectrum from L2 (one load in flight ahead of the
+// product), fused with the 8-point inverse DFT of inverse pass 0 in dit8's order
+template <typename T, bool COLD, typename AB>
+__device__ __forceinline__ void pointwise_dit8(CI<T> (&v)[8], const AB &A, int k0, int stride) {
+#ifndef IVM_NO_DIT8
+  CI<T> an = A.ld(k0);
+  dit8<T, true>(
+      v,
+      [&](int q) {
+        const CI<T> a = an;
+        const int nq = dit8_next(q);
+        if (nq >= 0) an = A.ld(nq * stride + k0);
+        return cmul_ss<T, COLD>(a, v[q]);
+      },
+      [] {});
+#else
+  CI<T> an = A.ld(k0);
+#pragma unroll
+  for (int r = 0; r < 8; r++) {
+    const CI<T> a = an;
+    if (r + 1 < 8) an = A.ld((r + 1) * stride + k0);
+    v[r] = cmul_ss<T, COLD>(a, v[r]);
+  }
+  cdft<T, 8, true>(v);
+#endif
+}
+
 // forward: F_p[k0][nu + Sp q] * w_{2LR}^{q(2k0+1)} -> R-point DFT
 template <typename T, int R>
 __device__ __forceinline__ void fwdR(Buf<T> st, const TwC<T> *twb, const PassRT &pp, CI<T> (&v)[R], int &k0,
@@ -652,6 +711,22 @@ __device__ __forceinline__ void fwdR(Buf<T> st, const TwC<T> *twb, const PassRT 
   nu = t & (Sp - 1);
   const int base = k0 * pp.RSi, sw = k0 & pp.SWi, tstride = pp.L >> 1;
   const TwC<T> *tp = twb + pp.tw + k0;
+#ifndef IVM_NO_DIT8
+  if constexpr (R == 8) {
+    dit8<T, false>(
+        v,
+        [&](int q) {
+          const CI<T> z = st.ld(base + ((nu + Sp * q) ^ sw));
+          if (q == 0) return z;
+          const TwC<T> w = tp[(q - 1) * tstride];
+          return (2 * q <= R) ? rtmul<T, false, false>(w, z) : rtmul<T, false, true>(w, z);
+        },
+        [&]() {
+          if (wbar) pb_arrive_warp(wbar);
+        });
+    return;
+  }
+#endif
 #pragma unroll
   for (int q = 0; q < R; q++) {
     CI<T> z = st.ld(base + ((nu + Sp * q) ^ sw));
@@ -676,6 +751,28 @@ __device__ __forceinline__ void invR(Buf<T> st, const TwC<T> *twb, const PassRT 
   const int base = k0 * pp.RSi, sw = k0 & pp.SWi;
   // folded last pass: entries [q][k0] for q = 0..15, else [q-1][k0]
   const TwC<T> *tp = twb + pp.tw + k0 + (FOLD ? 0 : -pp.L);
+#ifndef IVM_NO_DIT8
+  if constexpr (R == 8) {
+    dit8<T, true>(
+        v,
+        [&](int q) {
+          const int qq = (2 * q < R) ? q : R - q;
+          if (2 * q < R) {
+            const CI<T> z = st.ld(base + ((nu + Sp * q) ^ sw));
+            if (q == 0 && !FOLD) return z;
+            const TwC<T> w = tp[q * pp.L];
+            return (FOLD || 4 * qq > R) ? rtmul<T, true, true>(w, z) : rtmul<T, true, false>(w, z);
+          }
+          const CI<T> d = st.ld(base + ((S - 1 - nu - Sp * q) ^ sw));
+          const TwC<T> w = tp[q * pp.L];
+          return (FOLD || 4 * qq > R) ? rtmul_cd<T, false, true>(w, d) : rtmul_cd<T, false, false>(w, d);
+        },
+        [&]() {
+          if (wbar) pb_arrive_warp(wbar);
+        });
+    return;
+  }
+#endif
 #pragma unroll
   for (int q = 0; q < R; q++) {
     CI<T> z;
@@ -870,15 +967,7 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
 #pragma unroll
           for (int r = 0; r < R; r++) A.st(r * (pp.L >> 1) + k0, v[r]);
         } else {  // last pass of b + pointwise + inverse pass 0
-          // A from L2, one load in flight ahead of the product
-          CI<T> an = A.ld(k0);
-#pragma unroll
-          for (int r = 0; r < R; r++) {
-            const CI<T> a = an;
-            if (r + 1 < R) an = A.ld((r + 1) * (pp.L >> 1) + k0);
-            v[r] = cmul_ss(a, v[r]);
-          }
-          cdft<T, R, true>(v);
+          pointwise_dit8<T, false>(v, A, k0, pp.L >> 1);
           __syncthreads();
           if (LAST16 && threadIdx.x == 0) {  // the folded inverse table replaces the forward-last one
             mbar_expect(&tbar, L16_BYTES);

@@ -433,14 +433,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v4_kernel(KParams kp) {
 #pragma unroll
           for (int r = 0; r < R; r++) A.st(r * (pp.L >> 1) + k0, v[r]);
         } else {  // last forward pass of b + pointwise + inverse pass 0
-          CI<T> an = A.ld(k0);
-#pragma unroll
-          for (int r = 0; r < R; r++) {
-            const CI<T> a = an;
-            if (r + 1 < R) an = A.ld((r + 1) * (pp.L >> 1) + k0);
-            v[r] = cmul_ss<T, true>(a, v[r]);
-          }
-          cdft<T, R, true>(v);
+          pointwise_dit8<T, true>(v, A, k0, pp.L >> 1);
           __syncthreads();
           if (threadIdx.x == 0) {  // inverse pass 3 table replaces the forward-last one
             mbar_expect(&tbar, EB * X::FLAST);

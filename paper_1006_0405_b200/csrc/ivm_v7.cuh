@@ -150,14 +150,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v7_kernel(KParams kp, Pipe7 g) {
 #pragma unroll
             for (int r = 0; r < R; r++) A.st(r * (pp.L >> 1) + k0, v[r]);
           } else {
-            CI<T> an = A.ld(k0);
-#pragma unroll
-            for (int r = 0; r < R; r++) {
-              const CI<T> a = an;
-              if (r + 1 < R) an = A.ld((r + 1) * (pp.L >> 1) + k0);
-              v[r] = cmul_ss<T, true>(a, v[r]);
-            }
-            cdft<T, R, true>(v);
+            pointwise_dit8<T, true>(v, A, k0, pp.L >> 1);
             __syncthreads();
             if (threadIdx.x == 0) {
               mbar_expect(&tbar, EB * X::FLAST);
@@ -213,14 +206,19 @@ __global__ void __launch_bounds__(512, 1) ivm_v7_kernel(KParams kp, Pipe7 g) {
         const int b = (int)threadIdx.x / B, kl = (int)threadIdx.x % B;
         CI<T> v[8];
 #pragma unroll
-        for (int a = 0; a < 8; a++) {
+        for (int a = 0; a < 8; a++) {  // (the L2 loads first: all eight in flight)
           const int q = C2 * a + b;
           const int src = (2 * q < C) ? 2 * q : 2 * C - 1 - 2 * q;
-          const CI<T> z = ldcg_ci(xch + (size_t)src * 4096 + (int)role * B + kl);
-          const TwC<T> w = twb[X::S_SWAP + q * B + kl];
-          v[a] = (2 * q < C) ? rtmul<T, true, true>(w, z) : rtmul_cd<T, false, true>(w, z);
+          v[a] = ldcg_ci(xch + (size_t)src * 4096 + (int)role * B + kl);
         }
-        cdft<T, 8, true>(v);
+        dit8<T, true>(
+            v,
+            [&](int a) {
+              const int q = C2 * a + b;
+              const TwC<T> w = twb[X::S_SWAP + q * B + kl];
+              return (2 * q < C) ? rtmul<T, true, true>(w, v[a]) : rtmul_cd<T, false, true>(w, v[a]);
+            },
+            [] {});
 #pragma unroll
         for (int r1 = 1; r1 < 8; r1++) {  // b is warp-uniform (B >= 32)
           const int j = b * r1;
