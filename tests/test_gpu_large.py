@@ -270,3 +270,37 @@ def test_large_m_carry_patterns(ctx, n):
     assert cert.all()
     for p in range(B):
         assert to_int(out[p]) == to_int(a[p]) * to_int(b[p]), p
+
+
+@pytest.mark.parametrize("n", [1024, 2048, 4096, 8192, 16384, 32768, 65536, 75000, 131072])
+def test_throughput_variants_match_diagnostic_kernels(ctx, n):
+    """The one-CTA, cluster and pipelined group kernels each have a throughput
+    variant compiled without the interval-dump / coefficient / unaligned-digit
+    paths (picked when the rows are aligned and no diagnostics are asked for).
+    Same arithmetic: products, flags, max radii and first failing indices must be
+    bit-identical to the diagnostic build's, and every certified product exact
+    (n = 131,072 is the largest size the library takes; its enclosures are tighter
+    than the paper's, so even past P:5's 75,000 digits pairs may certify: whatever
+    the flag, both builds must agree and an uncertified product must be zero)."""
+    import torch
+    kinds = np.array([0, 1, 2, 3])
+    a, b = inputs.pair_digits(0xFA57 + n, np.arange(4), n, kinds)
+    ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    assert ta.data_ptr() % 16 == 0 and tb.data_ptr() % 16 == 0
+    diag = ctx.multiply_diag(ta, tb, dump_pairs=[0])      # dump + coefficients: diagnostic kernel
+    fast = ctx.multiply_diag(ta, tb, coeffs=False)        # no dump, no coefficients: throughput kernel
+    p, c = ctx.multiply(ta, tb)
+    torch.cuda.synchronize()
+    for k in ("prod", "cert", "first_bad"):
+        assert torch.equal(diag[k], fast[k]), k
+    assert torch.equal(diag["max_radius"].view(torch.int64), fast["max_radius"].view(torch.int64))
+    assert torch.equal(p, fast["prod"]) and torch.equal(c, fast["cert"])
+    cert = c.cpu().numpy().astype(bool)
+    prod = p.cpu().numpy()
+    if n <= 75000:
+        assert cert.all()
+    for i in range(4):
+        if cert[i]:
+            assert to_int(prod[i]) == to_int(a[i]) * to_int(b[i]), i
+        else:
+            assert not prod[i].any()
