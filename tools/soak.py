@@ -35,6 +35,8 @@ def main():
         lg = int(rng.integers(0, 18))  # n ~ 2^lg .. 2^(lg+1)
         n = int(rng.integers(1 << lg, (2 << lg) if lg < 17 else 131073))
         n = min(n, 131072)
+        if n >= 16 and rng.random() < 0.5:
+            n -= n % 16  # 16-byte aligned rows: the throughput kernel variants
         maxb = max(1, min(600, 4_000_000 // n))
         B = int(rng.integers(1, maxb + 1))
         prec = ivm.F32 if (n <= 4096 and rng.random() < 0.2) else ivm.F64
