@@ -228,6 +228,19 @@ __global__ void __launch_bounds__(512, 1) ivm_v7_kernel(KParams kp, Pipe7 g) {
 #pragma unroll
         for (int r1 = 0; r1 < 8; r1++) st.st((r1 * C2 + b) * B + kl, v[r1]);
         __syncthreads();
+#ifndef IVM_NO_DISCARD
+        // this task was the only reader of its rows of the exchange (whole 128-byte
+        // lines: 4 consecutive kl), and the next writer is another launch's or the ring's
+        // next pair: drop the dirty lines from L2 instead of writing them back to HBM
+        if ((kl & 3) == 0) {
+#pragma unroll
+          for (int a = 0; a < 8; a++) {
+            const int q = C2 * a + b;
+            const int src = (2 * q < C) ? 2 * q : 2 * C - 1 - 2 * q;
+            asm volatile("discard.global.L2 [%0], 128;" ::"l"(xch + (size_t)src * 4096 + (int)role * B + kl) : "memory");
+          }
+        }
+#endif
       }
       {  // stage 2: task (r1, kl), DFT_C2 over b, untwist remainder, emit into the swap buffer
         constexpr int TASKS = 8 * B / 512;
