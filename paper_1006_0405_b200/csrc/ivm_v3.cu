@@ -117,8 +117,10 @@ static int v3_info_impl(LaunchInfo *li) {
   auto k = v3::ivm_v3_kernel<T, M, R>;
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) != cudaSuccess)
     return -1;
-  if constexpr (sizeof(T) == 8) {  // the throughput variant (v3_go)
-    if (cudaFuncSetAttribute(v3::ivm_v3_kernel<T, M, R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if constexpr (sizeof(T) == 8) {  // the throughput variants (v3_go)
+    if (cudaFuncSetAttribute(v3::ivm_v3_kernel<T, M, R, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)C::SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(v3::ivm_v3_kernel<T, M, R, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)C::SMEM) != cudaSuccess)
       return -1;
   }
@@ -139,13 +141,15 @@ int v3_info(int prec, int m, int radix, LaunchInfo *li) { IVM_V3_DISPATCH(v3_inf
 
 template <typename T, int M, int R> static void v3_go(const KParams &kp, int grid, cudaStream_t s) {
   using C = v3::Cfg3<T, M, R>;
-  // fp64 with 16-byte aligned digit rows and no diagnostic outputs: the kernel
-  // compiled without the unstaged-digit and dump paths (same arithmetic)
+  // fp64 and no diagnostic outputs: the kernels compiled without the dump / coefficient
+  // paths, with staged digits when every row is 16-byte aligned, else without the
+  // staging (same arithmetic)
   if constexpr (sizeof(T) == 8) {
     const bool aligned = kp.n % 16 == 0 &&
                          ((reinterpret_cast<uintptr_t>(kp.a) | reinterpret_cast<uintptr_t>(kp.b)) % 16 == 0);
-    if (aligned && !kp.dump_slot && !kp.coeffs) {
-      v3::ivm_v3_kernel<T, M, R, true><<<grid, C::THREADS, C::SMEM, s>>>(kp);
+    if (!kp.dump_slot && !kp.coeffs) {
+      if (aligned) v3::ivm_v3_kernel<T, M, R, 1><<<grid, C::THREADS, C::SMEM, s>>>(kp);
+      else v3::ivm_v3_kernel<T, M, R, 2><<<grid, C::THREADS, C::SMEM, s>>>(kp);
       return;
     }
   }

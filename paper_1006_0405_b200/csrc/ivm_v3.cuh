@@ -857,10 +857,12 @@ __device__ __forceinline__ double *diag_dump(const KParams &kp, int pair, int N)
   return s >= 0 ? kp.intervals + (size_t)s * N * 4 : nullptr;
 }
 
-// FAST: the host guarantees staged digits (16-byte aligned rows) and no diagnostic
-// outputs (interval dump, snapped coefficients), so those paths and the values they
-// keep live across the pair loop are compiled out of the throughput kernel
-template <typename T, int M, int R, bool FAST = false>
+// MODE 1, 2: the throughput kernels.  The host guarantees no diagnostic outputs
+// (interval dump, snapped coefficients) and picks 1 when every digit row is 16-byte
+// aligned (digits staged by bulk copies) and 2 when not (digits read through L2), so
+// the other paths and the values they keep live across the pair loop are compiled
+// out.  MODE 0 has every path (runtime choices).
+template <typename T, int M, int R, int MODE = 0>
 __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) ivm_v3_kernel(KParams kp) {
   using C = Cfg3<T, M, R>;
   using Gm = G3<M, R>;
@@ -893,8 +895,10 @@ __global__ void __launch_bounds__(Cfg3<T, M, R>::THREADS, Cfg3<T, M, R>::MINB) i
   constexpr int RATIO = 2 * N / Gm::LASTL();
   constexpr int QS = C::THREADS;  // coefficient layout of the 4-words-per-thread carry (cpos)
   // digits staged by bulk copies when every row is 16-byte aligned
+  constexpr bool FAST = MODE != 0;
   const bool staged =
-      FAST || ((n % 16 == 0) && ((reinterpret_cast<uintptr_t>(kp.a) | reinterpret_cast<uintptr_t>(kp.b)) % 16 == 0));
+      MODE == 1 ||
+      (MODE == 0 && (n % 16 == 0) && ((reinterpret_cast<uintptr_t>(kp.a) | reinterpret_cast<uintptr_t>(kp.b)) % 16 == 0));
   if (threadIdx.x == 0) {
     mbar_init(&tbar);
     mbar_init(&dbar);

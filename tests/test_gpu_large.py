@@ -272,11 +272,12 @@ def test_large_m_carry_patterns(ctx, n):
         assert to_int(out[p]) == to_int(a[p]) * to_int(b[p]), p
 
 
-@pytest.mark.parametrize("n", [1024, 2048, 4096, 8192, 16384, 32768, 65536, 75000, 131072])
+@pytest.mark.parametrize("n", [500, 1000, 1024, 2048, 4088, 4096, 8192, 16384, 32768, 65536, 75000, 131072])
 def test_throughput_variants_match_diagnostic_kernels(ctx, n):
     """The one-CTA, cluster and pipelined group kernels each have a throughput
     variant compiled without the interval-dump / coefficient / unaligned-digit
-    paths (picked when the rows are aligned and no diagnostics are asked for).
+    paths (picked when no diagnostics are asked for; the one-CTA kernel has one for
+    16-byte aligned rows, with staged digits, and one for the rest: n = 500, 1000, 4088).
     Same arithmetic: products, flags, max radii and first failing indices must be
     bit-identical to the diagnostic build's, and every certified product exact
     (n = 131,072 is the largest size the library takes; its enclosures are tighter
