@@ -180,6 +180,11 @@ template <typename T, int M> static int v6_info_impl(LaunchInfo *li) {
   li->a_bytes_per_cta = C::A_BYTES;
   li->cluster = C::PPC;  // multiplications per CTA
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) != cudaSuccess) return -1;
+  if constexpr (sizeof(T) == 8) {
+    if (cudaFuncSetAttribute(v6::ivm_v6_kernel<T, M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)C::SMEM) != cudaSuccess)
+      return -1;
+  }
   int nb = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, C::THREADS, C::SMEM) != cudaSuccess) return -1;
   li->blocks_per_sm = nb;
@@ -196,6 +201,12 @@ int v6_info(int prec, int m, LaunchInfo *li) { IVM_V3_DISPATCH(v6_info_m, prec, 
 
 template <typename T, int M> static void v6_go(const KParams &kp, int grid, cudaStream_t s) {
   using C = v6::Cfg6<T, M>;
+  if constexpr (sizeof(T) == 8) {  // no diagnostic outputs: the kernel compiled without them
+    if (!kp.dump_slot && !kp.coeffs) {
+      v6::ivm_v6_kernel<T, M, true><<<grid, C::THREADS, C::SMEM, s>>>(kp);
+      return;
+    }
+  }
   v6::ivm_v6_kernel<T, M><<<grid, C::THREADS, C::SMEM, s>>>(kp);
 }
 template <int M> static int v6_launch_m(int prec, const KParams &kp, int grid, cudaStream_t s) {

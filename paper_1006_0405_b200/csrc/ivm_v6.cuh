@@ -110,7 +110,8 @@ __device__ __forceinline__ void carry_group(const int32_t *coef, int n, uint8_t 
   }
 }
 
-template <typename T, int M>
+// FAST: no diagnostic outputs (interval dump, snapped coefficients), host-checked
+template <typename T, int M, bool FAST = false>
 __global__ void __launch_bounds__(512, 1) ivm_v6_kernel(KParams kp) {
   using C = Cfg6<T, M>;
   using Gm = G3<M, 8>;
@@ -182,7 +183,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v6_kernel(KParams kp) {
         __syncwarp();
       }
     }
-    double *dump = valid ? diag_dump(kp, pair, N) : nullptr;
+    double *dump = (!FAST && valid) ? diag_dump(kp, pair, N) : nullptr;
 #pragma unroll 1
     for (int i = 0; i < NINV; i++) {
       const PassRT pp = (i == 0) ? X::inv(0) : X::inv(NINV > 1 ? 1 : 0);
@@ -210,7 +211,7 @@ __global__ void __launch_bounds__(512, 1) ivm_v6_kernel(KParams kp) {
     const bool certified = acc.ok != 0;
     carry_group<TPP>(coef, n, kp.prod + (size_t)pr * 2 * n, certified, valid);
     if (valid) {
-      if (kp.coeffs) {
+      if (!FAST && kp.coeffs) {
         int64_t *co = kp.coeffs + (size_t)pair * (2 * n - 1);
         for (int i = tid; i < 2 * n - 1; i += TPP) co[i] = certified ? coef[i] : 0;
       }

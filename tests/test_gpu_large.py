@@ -272,7 +272,7 @@ def test_large_m_carry_patterns(ctx, n):
         assert to_int(out[p]) == to_int(a[p]) * to_int(b[p]), p
 
 
-@pytest.mark.parametrize("n", [500, 1000, 1024, 2048, 4088, 4096, 8192, 16384, 32768, 65536, 75000, 131072])
+@pytest.mark.parametrize("n", [40, 100, 256, 500, 1000, 1024, 2048, 4088, 4096, 8192, 16384, 32768, 65536, 75000, 131072])
 def test_throughput_variants_match_diagnostic_kernels(ctx, n):
     """The one-CTA, cluster and pipelined group kernels each have a throughput
     variant compiled without the interval-dump / coefficient / unaligned-digit
