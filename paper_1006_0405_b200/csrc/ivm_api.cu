@@ -59,7 +59,7 @@ struct ivm_ctx {
   cudaEvent_t done_ev = nullptr;
   // co-run of the group kernel beside the cluster kernel (corun_split)
   bool corun = true;
-  double corun_eff = 0.8;
+  double corun_eff = 0.0;  // group kernel's rate relative to a cluster's; 0: the measured default per m
   cudaStream_t s_co = nullptr;
   cudaEvent_t co_ev[2] = {nullptr, nullptr};
   cudaStream_t last_stream = nullptr;
@@ -637,7 +637,10 @@ int ivm_multiply_batched_diag(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, s
     if (c->corun && cl == (size_t)li.max_clusters && get_info5(c, m, prec, &l5) == IVM_OK && l5.blocks_per_sm >= 1) {
       const size_t used = cl * C, free_sms = (size_t)c->sms > used ? (size_t)c->sms - used : 0;
       g5 = free_sms / C;
-      b5 = corun_split(batch, cl, g5, c->corun_eff);
+      // measured same-box sweeps: m = 2^15 (4 groups of 4 beside 33 clusters)
+      // 0.74, m = 2^16 (2 groups of 8 beside 16 clusters) 0.9
+      const double eff = c->corun_eff > 0.0 ? c->corun_eff : (m == 15 ? 0.74 : 0.9);
+      b5 = corun_split(batch, cl, g5, eff);
     }
     const size_t b4 = batch - b5;
     const size_t a4 = cl * C * li.a_bytes_per_cta;
