@@ -96,7 +96,10 @@ int ivm_multiply(ivm_ctx_t ctx, const uint8_t *a, const uint8_t *b, size_t n,
                  uint8_t *prod, uint8_t *certified, int prec, void *cuda_stream);
 
 /* Batched independent multiplications: a, b [batch][n], prod [batch][2n],
- * certified [batch] (all device pointers). */
+ * certified [batch] (all device pointers).  Any alignment and any n are
+ * accepted and give the same results; rows that are 16-byte aligned (a, b
+ * 16-byte aligned and n a multiple of 16) take the staged-digit kernels
+ * (bulk copies into shared memory one pair ahead), the fastest path. */
 int ivm_multiply_batched(ivm_ctx_t ctx, const uint8_t *a, const uint8_t *b, size_t n,
                          size_t batch, uint8_t *prod, uint8_t *certified, int prec,
                          void *cuda_stream);
