@@ -305,3 +305,19 @@ def test_throughput_variants_match_diagnostic_kernels(ctx, n):
             assert to_int(prod[i]) == to_int(a[i]) * to_int(b[i]), i
         else:
             assert not prod[i].any()
+
+
+@pytest.mark.parametrize("n,bound", [(1000, 1.55), (4096, 1.35), (16384, 1.25), (75000, 0.75)])
+def test_radius_tightness_per_size(ctx, n, bound):
+    """Tightness regression (SURVEY hard part 1): per pair, GPU max radius / oracle max
+    radius stays at the measured level (profiles/r02/radius_ratios.json: C1 1.45, C2
+    <= 1.27, C5 <= 1.14, C3 <= 0.56), well inside the north-star's 2x.  The excess over 1
+    at small m is the output-side untwist of the half-spectrum transform (R13)."""
+    B = 4 if n <= 16384 else 2
+    kinds = np.array([0, 0, 3, 3])[:B]  # uniform digits (all-255 ratios are lower)
+    a, b = inputs.pair_digits(0x71D + n, np.arange(B), n, kinds)
+    g = gpu_run(ctx, a, b)
+    r = oracle.ivmul(a, b)
+    assert g["cert"].all() and r["cert"].all()
+    ratio = g["max_radius"] / r["max_radius"]
+    assert np.all(ratio <= bound), (n, ratio)
