@@ -29,6 +29,7 @@ struct ivm_ctx {
   bool force_v1 = false;
   bool force_v5 = false;   // IVM_KERNEL=v5: the group kernel also for m = 2^14 .. 2^16
   bool v7 = true;          // fp64 m = 2^17, 2^18: the pipelined group kernel (IVM_V7=0: the lockstep one)
+  bool disc3 = true;       // circular sets at m = 2^10, 2^13 on the radix-8 schedule (IVM_DISC3=0: radix 2)
   void *g7scratch = nullptr;  // its stage counters and per-pair ring
   size_t g7scratch_bytes = 0;
   std::map<std::pair<int, int>, void *> tw4;  // (log2m, prec) -> v4 role tables
@@ -185,6 +186,8 @@ int ivm_create(ivm_ctx_t *ctx, int device) {
   {
     const char *e = getenv("IVM_V7");
     c->v7 = !(e && strcmp(e, "0") == 0);
+    const char *d = getenv("IVM_DISC3");
+    c->disc3 = !(d && strcmp(d, "0") == 0);
   }
   {  // IVM_CORUN=0 disables the co-run; IVM_CORUN_EFF sets the group kernel's relative rate
     const char *e = getenv("IVM_CORUN");
@@ -1020,6 +1023,32 @@ int ivm_multiply_disc(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, size_t n,
   StreamOrder order(c, stream);
   if (!order.ok) return cuda_fail(c);
   const int lg = log2m_for(n);  // n = 1: m = 1 (no FFT stage)
+  if ((lg == 10 || lg == 13) && c->disc3) {
+    // the one-CTA odd-frequency radix-8 schedule in disc arithmetic (ivm_d3.cuh),
+    // on the rectangular kernels' tables (IVM_DISC3=0: the radix-2 kernel below)
+    const void *tw3;
+    ivm::LaunchInfo li;
+    int r = get_table3(c, lg, IVM_F64, &tw3);
+    if (r) return r;
+    if (ivm::d3_info(lg, &li) != 0 || li.blocks_per_sm < 1) return cuda_fail(c);
+    size_t grid = (size_t)c->sms * (size_t)li.blocks_per_sm;
+    if (grid > batch) grid = batch;
+    r = ensure_scratch(c, grid * li.a_bytes_per_cta);
+    if (r) return r;
+    ivm::KParams kp = {};
+    kp.a = a;
+    kp.b = b;
+    kp.prod = prod;
+    kp.cert = cert;
+    kp.n = (int)n;
+    kp.batch = (int)batch;
+    kp.tw = tw3;
+    kp.ascratch = c->ascratch;
+    kp.max_radius = max_radius;
+    if (ivm::d3_launch(lg, kp, (int)grid, (cudaStream_t)stream) != 0) return cuda_fail(c);
+    c->last_launches = 1;
+    return IVM_OK;
+  }
   void *w = nullptr;
   double rw = 0.0;
   auto it = c->twd.find(lg);

@@ -9,6 +9,7 @@
 #include "ivm_carry.cuh"
 #include "ivm_v3.cuh"
 #include "ivm_v6.cuh"
+#include "ivm_d3.cuh"
 #include "ivm_twc_host.h"
 
 namespace ivm {
@@ -219,6 +220,41 @@ template <int M> static int v6_launch_m(int prec, const KParams &kp, int grid, c
 }
 int v6_launch(int prec, int m, const KParams &kp, int grid, cudaStream_t s) {
   IVM_V3_DISPATCH(v6_launch_m, prec, kp, grid, s)
+}
+
+
+// ---- circular containment sets on the one-CTA radix-8 schedule (ivm_d3.cuh): m = 2^10, 2^13 ----
+template <int M> static int d3_info_m(LaunchInfo *li) {
+  using C = d3::CfgD<M>;
+  auto k = d3::ivm_d3_kernel<M>;
+  li->threads = C::THREADS;
+  li->smem = C::SMEM;
+  li->a_smem = false;
+  li->a_bytes_per_cta = C::A_BYTES;
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) != cudaSuccess) return -1;
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, C::THREADS, C::SMEM) != cudaSuccess) return -1;
+  li->blocks_per_sm = nb;
+  return 0;
+}
+int d3_info(int m, LaunchInfo *li) {
+  switch (m) {
+    case 10: return d3_info_m<10>(li);
+    case 13: return d3_info_m<13>(li);
+    default: return -4;
+  }
+}
+template <int M> static int d3_go(const KParams &kp, int grid, cudaStream_t s) {
+  using C = d3::CfgD<M>;
+  d3::ivm_d3_kernel<M><<<grid, C::THREADS, C::SMEM, s>>>(kp);
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
+}
+int d3_launch(int m, const KParams &kp, int grid, cudaStream_t s) {
+  switch (m) {
+    case 10: return d3_go<10>(kp, grid, s);
+    case 13: return d3_go<13>(kp, grid, s);
+    default: return -4;
+  }
 }
 
 }  // namespace ivm

@@ -24,7 +24,7 @@ def run(ctx, a, b):
     return p.cpu().numpy(), c.cpu().numpy().astype(bool), r.cpu().numpy()
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 31, 100, 513, 1000, 2048, 4096])
+@pytest.mark.parametrize("n", [1, 2, 3, 31, 100, 257, 300, 512, 513, 1000, 2048, 2049, 3000, 4096])
 def test_disc_parity_with_oracle(ctx, n):
     K = inputs.KINDS
     B = 12
@@ -121,3 +121,33 @@ def test_disc_group_batch_deterministic(ctx):
     p2, c2, r2 = run(ctx, a, b)
     assert np.array_equal(p1, p2) and np.array_equal(c1, c2) and np.array_equal(r1, r2)
     assert c1.all() and oracle.residue_check(a, b, p1).all()
+
+
+@pytest.mark.parametrize("n", [300, 512, 2049, 4096])
+def test_disc_radix8_kernel_against_radix2_kernel(n, monkeypatch):
+    """m = 2^10 and 2^13 run the one-CTA odd-frequency radix-8 schedule in disc
+    arithmetic (csrc/ivm_d3.cuh); IVM_DISC3=0 keeps the paper's radix-2 DIT
+    (csrc/ivm_disc.cu).  Different FFT schedules, same products and flags on
+    certifiable inputs, radii within 2x of each other; a batch larger than the
+    grid, all digit kinds."""
+    import torch
+    import paper_1006_0405_b200 as ivm
+    B = 700
+    kinds = np.arange(B) % 4
+    a, b = inputs.pair_digits(0xD3 + n, np.arange(B), n, kinds)
+    ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    res = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("IVM_DISC3", flag)
+        c = ivm.Context(0)
+        p, ce, r = c.multiply_disc(ta, tb)
+        torch.cuda.synchronize()
+        res[flag] = (p.cpu().numpy(), ce.cpu().numpy().astype(bool), r.cpu().numpy())
+        c.close()
+    assert res["1"][1].all() and res["0"][1].all()
+    assert np.array_equal(res["1"][0], res["0"][0])
+    sel = np.arange(0, B, 53)
+    assert np.array_equal(res["1"][0][sel], oracle.long_multiply(a[sel], b[sel]))
+    ratio = np.maximum(res["1"][2], 1e-30) / np.maximum(res["0"][2], 1e-30)
+    assert (ratio <= 2.0).all() and (ratio >= 0.25).all(), (ratio.min(), ratio.max())
+    print("radix-8 / radix-2 disc radius", n, ratio.min(), ratio.max())
