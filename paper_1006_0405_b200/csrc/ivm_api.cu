@@ -29,7 +29,7 @@ struct ivm_ctx {
   bool force_v1 = false;
   bool force_v5 = false;   // IVM_KERNEL=v5: the group kernel also for m = 2^14 .. 2^16
   bool v7 = true;          // fp64 m = 2^17, 2^18: the pipelined group kernel (IVM_V7=0: the lockstep one)
-  bool disc3 = true;       // circular sets at m = 2^10, 2^13 on the radix-8 schedule (IVM_DISC3=0: radix 2)
+  bool disc3 = true;       // circular sets at m = 2^10 .. 2^13 on the radix-8 schedule (IVM_DISC3=0: radix 2)
   void *g7scratch = nullptr;  // its stage counters and per-pair ring
   size_t g7scratch_bytes = 0;
   std::map<std::pair<int, int>, void *> tw4;  // (log2m, prec) -> v4 role tables
@@ -1023,7 +1023,7 @@ int ivm_multiply_disc(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, size_t n,
   StreamOrder order(c, stream);
   if (!order.ok) return cuda_fail(c);
   const int lg = log2m_for(n);  // n = 1: m = 1 (no FFT stage)
-  if ((lg == 10 || lg == 13) && c->disc3) {
+  if (lg >= 10 && lg <= 13 && c->disc3) {
     // the one-CTA odd-frequency radix-8 schedule in disc arithmetic (ivm_d3.cuh),
     // on the rectangular kernels' tables (IVM_DISC3=0: the radix-2 kernel below)
     const void *tw3;

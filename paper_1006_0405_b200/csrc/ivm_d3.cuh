@@ -1,7 +1,6 @@
 // ivm_d3.cuh -- circular containment sets (R15) on the one-CTA
 // odd-frequency radix-8 schedule of ivm_v3.cuh (included by ivm_v3.cu): fp64,
-// m = 2^10 and 2^13 (the plans whose last inverse pass is radix 8; the other
-// sizes keep the radix-2 kernels of ivm_disc.cu).
+// m = 2^10 .. 2^13 (the other sizes keep the radix-2 kernels of ivm_disc.cu).
 //
 // Same transform, plans, index rules, tables and carry as ivm_v3_kernel; what
 // changes is the element: a disc <c, r> = { z : |z - c| <= r } instead of a
@@ -138,6 +137,22 @@ __device__ __forceinline__ void ddit8(DI (&v)[8], IN &&in) {
   v[0] = a0, v[1] = a1, v[2] = a2, v[3] = a3, v[4] = a4, v[5] = a5, v[6] = a6, v[7] = a7;
 }
 
+// R-point DFT of DIT butterflies, R = 2, 4 (cdft of ivm_v3.cuh)
+template <int R, bool INV>
+__device__ __forceinline__ void dcdft(DI (&v)[R]) {
+  static_assert(R == 2 || R == 4, "small first / last radices");
+  if constexpr (R == 2) {
+    dbfly(v[0], v[1], DI(v[1]));
+  } else {
+    DI a0 = v[0], a1 = v[2], a2 = v[1], a3 = v[3];
+    dbfly(a0, a1, DI(a1));
+    dbfly(a2, a3, DI(a3));
+    dbfly(a0, a2, DI(a2));
+    dbfly(a1, a3, dctw<INV>(a3, 1, 4));
+    v[0] = a0, v[1] = a1, v[2] = a2, v[3] = a3;
+  }
+}
+
 // state planes: centers (16 B) and radii (binary32, rounded up)
 struct BufD {
   double2 *c;
@@ -158,7 +173,6 @@ struct BufD {
 
 template <int M> struct CfgD {
   using Gm = G3<M, 8>;
-  static_assert(RT3<M, 8>::LAST16, "plans whose last inverse pass is radix 8");
   static constexpr int N = Gm::N, THREADS = Gm::THREADS, CAP = Gm::CAP;
   static constexpr int MINB = 512 / THREADS < 1 ? 1 : 512 / THREADS;
   static constexpr size_t STATE_BYTES = (size_t)CAP * 16 + (size_t)CAP * 4;
@@ -188,7 +202,8 @@ __global__ void __launch_bounds__(CfgD<M>::THREADS, CfgD<M>::MINB) ivm_d3_kernel
   constexpr int NFWD = RT3<M, R>::NFWD, NINV = RT3<M, R>::NINV;
   constexpr int RSI1 = Gm::iRS(1), SWI1 = Gm::iSW(1);
   constexpr unsigned FL_BYTES = sizeof(TwC<double>) * Gm::FLAST_ENT();
-  constexpr unsigned L16_BYTES = sizeof(TwC<double>) * R * Gm::LASTL();
+  constexpr bool LAST16 = RT3<M, R>::LAST16;
+  constexpr unsigned L16_BYTES = LAST16 ? sizeof(TwC<double>) * R * Gm::LASTL() : 0;
   constexpr unsigned SMF_BYTES = sizeof(TwC<double>) * Gm::SMF_ENT(), SMI_BYTES = sizeof(TwC<double>) * Gm::SMI_ENT();
   constexpr int RATIO = 2 * N / Gm::LASTL();
   constexpr int QS = C::THREADS;
@@ -213,25 +228,35 @@ __global__ void __launch_bounds__(CfgD<M>::THREADS, CfgD<M>::MINB) ivm_d3_kernel
     }
 #pragma unroll 1
     for (int op = 0; op < 2; op++) {
-      {  // pass 1 (ivm_v3.cuh fwd_first, R = 8): x[nu + S' q] w_32^q, 8-point DFT, mirror stores
-        constexpr int S = N / 2, Sp = S / R, L = 2;
+      {  // pass 1 (ivm_v3.cuh fwd_first): x[nu + S' q] w_{4 R1}^q, R1-point DFT, mirror stores
+        constexpr int R1 = Gm::P.f[1], G1 = R / R1, S = N / 2, Sp = S / R1, L = 2;
         constexpr int RSo = Gm::fRS(2), SWo = Gm::fSW(2);
         const uint8_t *dig = (op == 0 ? kp.a : kp.b) + (size_t)pair * n;
-        const int nu = (int)threadIdx.x;
-        DI v[R];
-        ddit8<false>(v, [&](int q) {
+        auto in1 = [&](int nu, int q) {
           const int idx = nu + Sp * q;
           const double x = digit_val<double>(idx < n ? (unsigned)dig[idx] : 0u);
           if (q == 0) return DI{x, 0.0, 0.0};
-          const TwC<double> w = cw64<double>(q * (16 / R));
+          const TwC<double> w = cw64<double>(q * (16 / R1));
           DI p{__dmul_rn(w.c, x), __dmul_rn(w.s, x), 0.0};
           p.r = __fma_ru(x, DRW, __fma_ru(DU, l1(p), 2 * DETA));
           return p;
-        });
+        };
 #pragma unroll
-        for (int r = 0; r < R; r++) {
-          if (r < R / 2) st.st(sidx(L * r, nu, RSo, SWo), v[r]);
-          else st.st_conj(sidx(L * R - 1 - L * r, nu, RSo, SWo), v[r]);
+        for (int g = 0; g < G1; g++) {
+          const int nu = (int)threadIdx.x + g * Gm::TASKS;
+          DI v[R1];
+          if constexpr (R1 == 8) {
+            ddit8<false>(v, [&](int q) { return in1(nu, q); });
+          } else {
+#pragma unroll
+            for (int q = 0; q < R1; q++) v[q] = in1(nu, q);
+            dcdft<R1, false>(v);
+          }
+#pragma unroll
+          for (int r = 0; r < R1; r++) {
+            if (r < R1 / 2) st.st(sidx(L * r, nu, RSo, SWo), v[r]);
+            else st.st_conj(sidx(L * R1 - 1 - L * r, nu, RSo, SWo), v[r]);
+          }
         }
       }
       if (op == 1 && threadIdx.x == 0) {
@@ -243,7 +268,7 @@ __global__ void __launch_bounds__(CfgD<M>::THREADS, CfgD<M>::MINB) ivm_d3_kernel
 #pragma unroll
       for (int i = 0; i < NFWD; i++) {
         const PassRT pp = pick_fwd<M, R>(i);
-        if (op == 0 && pp.big) mbar_wait(&tbar, 0);  // forward-last table restored
+        if (LAST16 && op == 0 && pp.big) mbar_wait(&tbar, 0);  // forward-last table restored
         const int Sp = 1 << pp.lgSp, t = (int)threadIdx.x;
         const int k0 = t >> pp.lgSp, nu = t & (Sp - 1);
         const int base = k0 * pp.RSi, sw = k0 & pp.SWi, tstride = pp.L >> 1;
@@ -275,7 +300,7 @@ __global__ void __launch_bounds__(CfgD<M>::THREADS, CfgD<M>::MINB) ivm_d3_kernel
             return dmul(a, v[q]);
           });
           __syncthreads();
-          if (threadIdx.x == 0) {  // the folded inverse table replaces the forward-last one
+          if (LAST16 && threadIdx.x == 0) {  // the folded inverse table replaces the forward-last one
             mbar_expect(&tbar, L16_BYTES);
             bulk_copy(twb, tw + Gm::tw_l16(), L16_BYTES, &tbar);
           }
@@ -290,7 +315,7 @@ __global__ void __launch_bounds__(CfgD<M>::THREADS, CfgD<M>::MINB) ivm_d3_kernel
 #pragma unroll
     for (int i = 0; i < NINV; i++) {
       const PassRT pp = pick_inv<M, R>(i);
-      const bool last = i == NINV - 1;
+      const bool last = LAST16 && i == NINV - 1;
       if (last) mbar_wait(&tbar, 1);  // folded table
       const int Sp = 1 << pp.lgSp, lgH = pp.lgSp - 1, S = R * Sp, t = (int)threadIdx.x;
       const int k0 = t >> lgH, nu = t & ((Sp >> 1) - 1);
@@ -329,9 +354,48 @@ __global__ void __launch_bounds__(CfgD<M>::THREADS, CfgD<M>::MINB) ivm_d3_kernel
       }
       __syncthreads();
     }
+    if constexpr (!LAST16) {  // last inverse pass of radix 2 or 4 (ivm_v3.cuh inv_last), tables from L2
+      constexpr int p = Gm::P.ni - 1, Q = Gm::P.q[p], L = iL(Gm::P, p), S = N / L, Sp = S / Q, G = R / Q;
+      constexpr int H = Sp / 2, RSi = Gm::iRS(p), SWi = Gm::iSW(p), TW = Gm::tw_inv(p), TWF = Gm::tw_fin();
+      static_assert(Gm::TASKS * G == L * H, "every thread has G tasks");
+      DI v[G][Q];
+      int k0s[G];
+#pragma unroll
+      for (int g = 0; g < G; g++) {
+        const int t = (int)threadIdx.x + g * Gm::TASKS;
+        const int k0 = t / H, nu = t % H;
+        k0s[g] = k0;
+#pragma unroll
+        for (int q = 0; q < Q; q++) {
+          if (2 * q < Q) {
+            const DI z = st.ld(sidx(k0, nu + Sp * q, RSi, SWi));
+            v[g][q] = q > 0 ? drt<true, true>(ldg_twc(tw, TW + (q - 1) * L + k0), z) : z;
+          } else {
+            const DI d = dconj(st.ld(sidx(k0, S - 1 - nu - Sp * q, RSi, SWi)));
+            v[g][q] = drt<false, true>(ldg_twc(tw, TW + (q - 1) * L + k0), d);
+          }
+        }
+        dcdft<Q, true>(v[g]);
+      }
+      __syncthreads();  // every input loaded: the coefficients may overwrite the state
+#pragma unroll
+      for (int g = 0; g < G; g++) {
+#pragma unroll
+        for (int r = 0; r < Q; r++) {
+          const int k = k0s[g] + L * r;
+          // (2/m) z^{-k}: the conjugate of the (scaled) table entry (emit_coeffs)
+          const DI w = drt<true, true, true>(ldg_twc(tw, TWF + k), v[g][r], SCALE);
+          certify_real<double, int32_t, false>(__dadd_rd(w.cr, -w.r), __dadd_ru(w.cr, w.r), k, n, coef + cpos<QS>(k), acc,
+                                               nullptr);
+          certify_real<double, int32_t, false>(__dadd_rd(w.ci, -w.r), __dadd_ru(w.ci, w.r), k + N / 2, n,
+                                               coef + cpos<QS>(k + N / 2), acc, nullptr);
+        }
+      }
+      __syncthreads();
+    }
     cert_flush(acc, cs);
     __syncthreads();
-    if (threadIdx.x == 0 && nxt < kp.batch) {  // restore the forward-last table
+    if (LAST16 && threadIdx.x == 0 && nxt < kp.batch) {  // restore the forward-last table
       mbar_expect(&tbar, FL_BYTES);
       bulk_copy(twb, tw + Gm::tw_fwd(Gm::P.nf - 1), FL_BYTES, &tbar);
     }

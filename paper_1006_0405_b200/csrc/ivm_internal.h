@@ -49,7 +49,7 @@ int v3_launch(int prec, int m, int radix, const KParams &kp, int grid, cudaStrea
 // small m (2^6 .. 2^9): 8192/m multiplications per 512-thread CTA
 int v6_info(int prec, int m, LaunchInfo *li);
 int v6_launch(int prec, int m, const KParams &kp, int grid, cudaStream_t s);
-// circular containment sets on the one-CTA radix-8 schedule: m = 2^10, 2^13 (fp64)
+// circular containment sets on the one-CTA radix-8 schedule: m = 2^10 .. 2^13 (fp64)
 int d3_info(int m, LaunchInfo *li);
 int d3_launch(int m, const KParams &kp, int grid, cudaStream_t s);
 // m = 2^14 .. 2^16: one thread-block cluster of m/8192 CTAs per multiplication

@@ -223,7 +223,7 @@ int v6_launch(int prec, int m, const KParams &kp, int grid, cudaStream_t s) {
 }
 
 
-// ---- circular containment sets on the one-CTA radix-8 schedule (ivm_d3.cuh): m = 2^10, 2^13 ----
+// ---- circular containment sets on the one-CTA radix-8 schedule (ivm_d3.cuh): m = 2^10 .. 2^13 ----
 template <int M> static int d3_info_m(LaunchInfo *li) {
   using C = d3::CfgD<M>;
   auto k = d3::ivm_d3_kernel<M>;
@@ -240,6 +240,8 @@ template <int M> static int d3_info_m(LaunchInfo *li) {
 int d3_info(int m, LaunchInfo *li) {
   switch (m) {
     case 10: return d3_info_m<10>(li);
+    case 11: return d3_info_m<11>(li);
+    case 12: return d3_info_m<12>(li);
     case 13: return d3_info_m<13>(li);
     default: return -4;
   }
@@ -252,6 +254,8 @@ template <int M> static int d3_go(const KParams &kp, int grid, cudaStream_t s) {
 int d3_launch(int m, const KParams &kp, int grid, cudaStream_t s) {
   switch (m) {
     case 10: return d3_go<10>(kp, grid, s);
+    case 11: return d3_go<11>(kp, grid, s);
+    case 12: return d3_go<12>(kp, grid, s);
     case 13: return d3_go<13>(kp, grid, s);
     default: return -4;
   }

@@ -123,9 +123,9 @@ def test_disc_group_batch_deterministic(ctx):
     assert c1.all() and oracle.residue_check(a, b, p1).all()
 
 
-@pytest.mark.parametrize("n", [300, 512, 2049, 4096])
+@pytest.mark.parametrize("n", [300, 512, 777, 1024, 1500, 2048, 2049, 4096])
 def test_disc_radix8_kernel_against_radix2_kernel(n, monkeypatch):
-    """m = 2^10 and 2^13 run the one-CTA odd-frequency radix-8 schedule in disc
+    """m = 2^10 .. 2^13 run the one-CTA odd-frequency radix-8 schedule in disc
     arithmetic (csrc/ivm_d3.cuh); IVM_DISC3=0 keeps the paper's radix-2 DIT
     (csrc/ivm_disc.cu).  Different FFT schedules, same products and flags on
     certifiable inputs, radii within 2x of each other; a batch larger than the
