@@ -236,11 +236,15 @@ def run_reference(args):
 def time_config(ctx, cfg, steps, flush, dev):
     """Device time of one other config on this rank (N = 1 runs): the same
     protocol as the main measurement (inputs resident, L2 flushed outside the
-    events, warm-up first); returns its summary for the line's other_configs."""
+    events, warm-up first); returns its summary for the line's other_configs.
+    "<cfg>-disc": the same workload with circular containment sets (P:290,
+    ivm_multiply_disc) instead of the rectangular ones."""
     import numpy as np
     import torch
     import paper_1006_0405_b200 as ivm
     from paper_1006_0405_b200 import inputs
+    disc = cfg.endswith("-disc")
+    cfg = cfg[:-5] if disc else cfg
     n, batch, prec_s, kind, _ = CONFIGS[cfg]
     seed = inputs.config_seed(int(cfg[1:]))
     if isinstance(kind, str):
@@ -249,8 +253,12 @@ def time_config(ctx, cfg, steps, flush, dev):
     b = ctx.generate_digits(n, batch, seed, 1, kind=kind)
     out = torch.empty((batch, 2 * n), dtype=torch.uint8, device=dev)
     cert = torch.empty((batch,), dtype=torch.uint8, device=dev)
+    if disc:
+        mul = lambda: ctx.multiply_disc(a, b, out=out, cert=cert, want_radius=False)
+    else:
+        mul = lambda: ctx.multiply(a, b, out=out, cert=cert)
     for _ in range(3):
-        ctx.multiply(a, b, out=out, cert=cert)
+        mul()
     torch.cuda.synchronize()
     s = torch.cuda.current_stream()
     ms = []
@@ -260,7 +268,7 @@ def time_config(ctx, cfg, steps, flush, dev):
         flush.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s)
-        ctx.multiply(a, b, out=out, cert=cert)
+        mul()
         e1.record(s)
         torch.cuda.synchronize()
         ms.append(e0.elapsed_time(e1))
@@ -270,7 +278,7 @@ def time_config(ctx, cfg, steps, flush, dev):
     m = ivm.fft_length(n)
     peaks = load_peaks()
     peak_ops = 148 * 64 * peaks.get("sm_max_mhz", 1965.0) * 1e6
-    r = {"workload": CONFIGS[cfg][4], "ms_per_step": t, "steps": steps, "value": ncert * n / (t / 1e3),
+    r = {"workload": CONFIGS[cfg][4] + (" -- circular containment sets (P:290)" if disc else ""), "ms_per_step": t, "steps": steps, "value": ncert * n / (t / 1e3),
          "unit": UNIT, "certified_pairs": ncert, "batch": batch,
          "roofline_frac": W_ops(m) * batch / (t / 1e3) / peak_ops, "gpu_launches_per_step": ctx.last_launch_count,
          "clocks": clocks}
@@ -486,7 +494,7 @@ def main():
     ap.add_argument("--gather", action="store_true",
                     help="also time the step with the products gathered to rank 0 (pipelined NCCL sends)")
     ap.add_argument("--gather-chunks", type=int, default=4)
-    ap.add_argument("--other-configs", default="C1,C3,C5",
+    ap.add_argument("--other-configs", default="C1,C3,C5,C2-disc",
                     help="at N = 1 also time these configs (same protocol) into the line's other_configs; '' for none")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
