@@ -1049,6 +1049,33 @@ int ivm_multiply_disc(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, size_t n,
     c->last_launches = 1;
     return IVM_OK;
   }
+  if ((lg == 14 || lg == 15) && c->disc3 && n % 16 == 0 &&
+      ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) % 16) == 0) {
+    // the cluster schedule in disc arithmetic (ivm_d4.cuh), on the rectangular cluster
+    // kernel's tables; unaligned rows keep the radix-2 group kernel below
+    const void *tw4;
+    ivm::LaunchInfo li;
+    int r = get_table4(c, lg, IVM_F64, &tw4);
+    if (r) return r;
+    if (ivm::d4_info(lg, &li) != 0 || li.max_clusters < 1) return cuda_fail(c);
+    size_t cl = (size_t)li.max_clusters;
+    if (cl > batch) cl = batch;
+    r = ensure_scratch(c, cl * (size_t)li.cluster * li.a_bytes_per_cta);
+    if (r) return r;
+    ivm::KParams kp = {};
+    kp.a = a;
+    kp.b = b;
+    kp.prod = prod;
+    kp.cert = cert;
+    kp.n = (int)n;
+    kp.batch = (int)batch;
+    kp.tw = tw4;
+    kp.ascratch = c->ascratch;
+    kp.max_radius = max_radius;
+    if (ivm::d4_launch(lg, kp, (int)cl, (cudaStream_t)stream) != 0) return cuda_fail(c);
+    c->last_launches = 1;
+    return IVM_OK;
+  }
   void *w = nullptr;
   double rw = 0.0;
   auto it = c->twd.find(lg);

@@ -10,6 +10,8 @@
 #include "ivm_carry.cuh"
 #include "ivm_v3.cuh"
 #include "ivm_v4.cuh"
+#include "ivm_d3.cuh"
+#include "ivm_d4.cuh"
 #include "ivm_twc_host.h"
 
 namespace ivm {
@@ -224,6 +226,61 @@ template <int M> static int v4_launch_m(int prec, const KParams &kp, int cluster
 }
 int v4_launch(int prec, int m, const KParams &kp, int clusters, cudaStream_t s) {
   IVM_V4_DISPATCH(v4_launch_m, prec, kp, clusters, s)
+}
+
+
+// ---- circular containment sets on the cluster schedule (ivm_d4.cuh): fp64, m = 2^14, 2^15 ----
+template <int M> static void d4_cfg(cudaLaunchConfig_t &cfg, cudaLaunchAttribute *attr, int clusters, cudaStream_t s) {
+  using CF = d4::CfgD4<M>;
+  constexpr int C = v4::G4<M>::C;
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(C * clusters);
+  cfg.blockDim = dim3(CF::THREADS);
+  cfg.dynamicSmemBytes = CF::SMEM;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+}
+template <int M> static int d4_info_m(LaunchInfo *li) {
+  using CF = d4::CfgD4<M>;
+  auto k = d4::ivm_d4_kernel<M>;
+  li->threads = CF::THREADS;
+  li->smem = CF::SMEM;
+  li->a_smem = false;
+  li->a_bytes_per_cta = CF::A_BYTES;
+  li->cluster = v4::G4<M>::C;
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM) != cudaSuccess) return -1;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  d4_cfg<M>(cfg, attr, 64, nullptr);
+  int ncl = 0;
+  if (cudaOccupancyMaxActiveClusters(&ncl, (void *)k, &cfg) != cudaSuccess) return -1;
+  li->blocks_per_sm = ncl > 0 ? 1 : 0;
+  li->max_clusters = ncl;
+  return 0;
+}
+int d4_info(int m, LaunchInfo *li) {
+  switch (m) {
+    case 14: return d4_info_m<14>(li);
+    case 15: return d4_info_m<15>(li);
+    default: return -4;
+  }
+}
+template <int M> static int d4_go(const KParams &kp, int clusters, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  d4_cfg<M>(cfg, attr, clusters, s);
+  return cudaLaunchKernelEx(&cfg, d4::ivm_d4_kernel<M>, kp) == cudaSuccess ? 0 : -1;
+}
+int d4_launch(int m, const KParams &kp, int clusters, cudaStream_t s) {
+  switch (m) {
+    case 14: return d4_go<14>(kp, clusters, s);
+    case 15: return d4_go<15>(kp, clusters, s);
+    default: return -4;
+  }
 }
 
 }  // namespace ivm

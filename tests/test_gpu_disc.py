@@ -75,10 +75,11 @@ def test_disc_rejects_too_large(ctx):
         ctx.multiply_disc(t, t)
 
 
-@pytest.mark.parametrize("n", [4097, 5000, 8193, 12000, 20000, 40000])
+@pytest.mark.parametrize("n", [4097, 4112, 5000, 6000, 8192, 8193, 8208, 12000, 16384, 20000, 40000])
 def test_disc_group_parity_with_oracle(ctx, n):
-    """m = 2^14 .. 2^17: the group kernel (8192 x m/8192 DIT factorization)
-    against the disc oracle: products bit-exact, flags where the oracle
+    """m = 2^14 .. 2^17: the cluster kernel in disc arithmetic (m = 2^14, 2^15,
+    n a multiple of 16: ivm_d4.cuh) and the radix-2 group kernel (8192 x m/8192
+    DIT factorization; the other sizes) against the disc oracle: products bit-exact, flags where the oracle
     certifies with margin, radius within 2x (and not below 1/4)."""
     K = inputs.KINDS
     kinds = np.array([K["uniform"], K["all255"], K["sparse"], K["msd"]])
@@ -151,3 +152,34 @@ def test_disc_radix8_kernel_against_radix2_kernel(n, monkeypatch):
     ratio = np.maximum(res["1"][2], 1e-30) / np.maximum(res["0"][2], 1e-30)
     assert (ratio <= 2.0).all() and (ratio >= 0.25).all(), (ratio.min(), ratio.max())
     print("radix-8 / radix-2 disc radius", n, ratio.min(), ratio.max())
+
+
+@pytest.mark.parametrize("n,B", [(8192, 230), (16384, 120)])
+def test_disc_cluster_kernel_against_group_kernel(n, B, monkeypatch):
+    """m = 2^14, 2^15 with 16-byte aligned rows run the cluster schedule in disc
+    arithmetic (csrc/ivm_d4.cuh); IVM_DISC3=0 keeps the radix-2 group kernel.  A
+    batch of several pairs per cluster, all digit kinds: same products and flags,
+    radii within 2x of each other, a sample bit-exact against Python ints."""
+    import torch
+    import paper_1006_0405_b200 as ivm
+    kinds = np.arange(B) % 4
+    a, b = inputs.pair_digits(0xD4 + n, np.arange(B), n, kinds)
+    ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    res = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("IVM_DISC3", flag)
+        c = ivm.Context(0)
+        p, ce, r = c.multiply_disc(ta, tb)
+        p2, ce2, r2 = c.multiply_disc(ta, tb)  # (a second call on the same context: deterministic)
+        torch.cuda.synchronize()
+        assert torch.equal(p, p2) and torch.equal(ce, ce2) and torch.equal(r, r2)
+        res[flag] = (p.cpu().numpy(), ce.cpu().numpy().astype(bool), r.cpu().numpy())
+        c.close()
+    assert res["1"][1].all() and res["0"][1].all()
+    assert np.array_equal(res["1"][0], res["0"][0])
+    big = lambda d: int.from_bytes(bytes(d), "little")
+    for i in range(0, B, 29):
+        assert big(res["1"][0][i]) == big(a[i]) * big(b[i]), i
+    ratio = np.maximum(res["1"][2], 1e-30) / np.maximum(res["0"][2], 1e-30)
+    assert (ratio <= 2.0).all() and (ratio >= 0.25).all(), (ratio.min(), ratio.max())
+    print("cluster / group disc radius", n, ratio.min(), ratio.max())
