@@ -450,7 +450,7 @@ static int v7_ring(size_t grid, size_t C, size_t batch, size_t pair_bytes) {
   return (int)rp;
 }
 static int launch_v7(ivm_ctx_t c, int m, const ivm::KParams &kp0, const ivm::LaunchInfo &li, size_t batch,
-                     cudaStream_t s) {
+                     cudaStream_t s, bool disc = false) {
   const size_t C = (size_t)li.cluster;
   size_t grid = (size_t)c->sms * li.blocks_per_sm;
   if (grid > batch * C) grid = batch * C;
@@ -481,7 +481,7 @@ static int launch_v7(ivm_ctx_t c, int m, const ivm::KParams &kp0, const ivm::Lau
   if (cudaMemsetAsync(pa.cnt, 0, b_cnt, s) != cudaSuccess) return cuda_fail(c);
   ivm::KParams kp = kp0;
   kp.ascratch = c->ascratch;
-  if (ivm::v7_launch(m, kp, pa, (int)grid, s) != 0) return cuda_fail(c);
+  if ((disc ? ivm::d7_launch(m, kp, pa, (int)grid, s) : ivm::v7_launch(m, kp, pa, (int)grid, s)) != 0) return cuda_fail(c);
   return IVM_OK;
 }
 
@@ -1073,6 +1073,29 @@ int ivm_multiply_disc(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, size_t n,
     kp.ascratch = c->ascratch;
     kp.max_radius = max_radius;
     if (ivm::d4_launch(lg, kp, (int)cl, (cudaStream_t)stream) != 0) return cuda_fail(c);
+    c->last_launches = 1;
+    return IVM_OK;
+  }
+  if ((lg == 17 || lg == 18) && c->disc3 && n % 4 == 0 &&
+      ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) % 4) == 0) {
+    // the pipelined group schedule in disc arithmetic (ivm_d7.cuh), on the rectangular
+    // kernel's tables and scratch layout; unaligned rows keep the radix-2 group kernel below
+    const void *tw4;
+    ivm::LaunchInfo li;
+    int r = get_table4(c, lg, IVM_F64, &tw4);
+    if (r) return r;
+    if (ivm::d7_info(lg, &li) != 0 || li.blocks_per_sm < 1) return cuda_fail(c);
+    ivm::KParams kp = {};
+    kp.a = a;
+    kp.b = b;
+    kp.prod = prod;
+    kp.cert = cert;
+    kp.n = (int)n;
+    kp.batch = (int)batch;
+    kp.tw = tw4;
+    kp.max_radius = max_radius;
+    r = launch_v7(c, lg, kp, li, batch, (cudaStream_t)stream, true);
+    if (r) return r;
     c->last_launches = 1;
     return IVM_OK;
   }

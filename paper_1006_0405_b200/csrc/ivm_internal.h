@@ -85,6 +85,9 @@ struct Pipe7Args {
 };
 int v7_info(int m, LaunchInfo *li);
 int v7_launch(int m, const KParams &kp, const Pipe7Args &pa, int grid, cudaStream_t s);
+// circular containment sets on the same pipeline (ivm_d7.cuh; word-aligned digit rows)
+int d7_info(int m, LaunchInfo *li);
+int d7_launch(int m, const KParams &kp, const Pipe7Args &pa, int grid, cudaStream_t s);
 
 // batch summary {certified count, max radius} into out[2] (device), zeroed first
 int summary_launch(const uint8_t *cert, const double *rad, int batch, double *out, cudaStream_t s);

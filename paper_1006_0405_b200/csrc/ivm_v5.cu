@@ -12,6 +12,8 @@
 #include "ivm_v4.cuh"
 #include "ivm_v5.cuh"
 #include "ivm_v7.cuh"
+#include "ivm_d3.cuh"
+#include "ivm_d7.cuh"
 #include "ivm_twc_host.h"
 
 namespace ivm {
@@ -133,6 +135,47 @@ int v7_launch(int m, const KParams &kp, const Pipe7Args &pa, int grid, cudaStrea
   switch (m) {
     case 17: return v7_go<17>(kp, pa, grid, s);
     case 18: return v7_go<18>(kp, pa, grid, s);
+    default: return -4;
+  }
+}
+
+
+// ---- circular containment sets on the pipelined group schedule (ivm_d7.cuh): fp64, m = 2^17, 2^18 ----
+template <int M> static int d7_info_m(LaunchInfo *li) {
+  using CF = d7::CfgD7<M>;
+  auto k = d7::ivm_d7_kernel<M>;
+  li->threads = CF::THREADS;
+  li->smem = CF::SMEM;
+  li->a_smem = false;
+  li->a_bytes_per_cta = CF::A_BYTES;
+  li->cluster = v4::G4<M>::C;
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM) != cudaSuccess) return -1;
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, CF::THREADS, CF::SMEM) != cudaSuccess) return -1;
+  li->blocks_per_sm = nb > 1 ? 1 : nb;  // one CTA per SM (the persistent grid of ivm_v7.cuh)
+  li->max_clusters = 0;
+  return 0;
+}
+int d7_info(int m, LaunchInfo *li) {
+  switch (m) {
+    case 17: return d7_info_m<17>(li);
+    case 18: return d7_info_m<18>(li);
+    default: return -4;
+  }
+}
+template <int M> static int d7_go(const KParams &kp, const Pipe7Args &pa, int grid, cudaStream_t s) {
+  using CF = d7::CfgD7<M>;
+  KParams k2 = kp;
+  v7::Pipe7 g{pa.cnt, pa.xch, pa.wds, pa.rec, pa.link, pa.rp};
+  void *args[] = {(void *)&k2, (void *)&g};
+  const cudaError_t e = cudaLaunchCooperativeKernel((const void *)d7::ivm_d7_kernel<M>, dim3(grid), dim3(CF::THREADS),
+                                                    args, CF::SMEM, s);
+  return e == cudaSuccess ? 0 : -1;
+}
+int d7_launch(int m, const KParams &kp, const Pipe7Args &pa, int grid, cudaStream_t s) {
+  switch (m) {
+    case 17: return d7_go<17>(kp, pa, grid, s);
+    case 18: return d7_go<18>(kp, pa, grid, s);
     default: return -4;
   }
 }

@@ -154,11 +154,12 @@ def test_disc_radix8_kernel_against_radix2_kernel(n, monkeypatch):
     print("radix-8 / radix-2 disc radius", n, ratio.min(), ratio.max())
 
 
-@pytest.mark.parametrize("n,B", [(8192, 230), (16384, 120)])
+@pytest.mark.parametrize("n,B", [(8192, 230), (16384, 120), (40000, 40), (65536, 24), (75000, 20), (131072, 10)])
 def test_disc_cluster_kernel_against_group_kernel(n, B, monkeypatch):
     """m = 2^14, 2^15 with 16-byte aligned rows run the cluster schedule in disc
-    arithmetic (csrc/ivm_d4.cuh); IVM_DISC3=0 keeps the radix-2 group kernel.  A
-    batch of several pairs per cluster, all digit kinds: same products and flags,
+    arithmetic (csrc/ivm_d4.cuh), m = 2^17, 2^18 with word-aligned rows the pipelined
+    group schedule (csrc/ivm_d7.cuh); IVM_DISC3=0 keeps the radix-2 group kernel.  A
+    batch of several pairs per cluster / several tasks per CTA, all digit kinds: same products and flags,
     radii within 2x of each other, a sample bit-exact against Python ints."""
     import torch
     import paper_1006_0405_b200 as ivm
