@@ -1049,7 +1049,7 @@ int ivm_multiply_disc(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, size_t n,
     c->last_launches = 1;
     return IVM_OK;
   }
-  if ((lg == 14 || lg == 15) && c->disc3 && n % 16 == 0 &&
+  if (lg >= 14 && lg <= 16 && c->disc3 && n % 16 == 0 &&
       ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) % 16) == 0) {
     // the cluster schedule in disc arithmetic (ivm_d4.cuh), on the rectangular cluster
     // kernel's tables; unaligned rows keep the radix-2 group kernel below

@@ -137,11 +137,13 @@ __device__ __forceinline__ void ddit8(DI (&v)[8], IN &&in) {
   v[0] = a0, v[1] = a1, v[2] = a2, v[3] = a3, v[4] = a4, v[5] = a5, v[6] = a6, v[7] = a7;
 }
 
-// R-point DFT of DIT butterflies, R = 2, 4 (cdft of ivm_v3.cuh)
+// R-point DFT of DIT butterflies, R = 2, 4, 8 (cdft of ivm_v3.cuh)
 template <int R, bool INV>
 __device__ __forceinline__ void dcdft(DI (&v)[R]) {
-  static_assert(R == 2 || R == 4, "small first / last radices");
-  if constexpr (R == 2) {
+  static_assert(R == 2 || R == 4 || R == 8, "radices");
+  if constexpr (R == 8) {
+    ddit8<INV>(v, [&](int q) { return v[q]; });
+  } else if constexpr (R == 2) {
     dbfly(v[0], v[1], DI(v[1]));
   } else {
     DI a0 = v[0], a1 = v[2], a2 = v[1], a3 = v[3];

@@ -1,5 +1,5 @@
 // ivm_d4.cuh -- circular containment sets (R15) on the cluster
-// schedule of ivm_v4.cuh: fp64, m = 2^14 and 2^15, one thread-block cluster of
+// schedule of ivm_v4.cuh: fp64, m = 2^14 .. 2^16, one thread-block cluster of
 // C = m/8192 CTAs per multiplication, digits staged by bulk copies (16-byte
 // aligned rows; the host falls back to the radix-2 group kernel otherwise).
 // Included by ivm_v4.cu after ivm_v4.cuh and ivm_d3.cuh.
@@ -28,7 +28,7 @@ __device__ __forceinline__ float dsm_ld_f32(unsigned a) {
 
 template <int M> struct CfgD4 {
   using GL = G3<13, 8>;
-  static_assert(M == 14 || M == 15, "staged digits, C = 2, 4");
+  static_assert(M >= 14 && M <= 16, "C = 2, 4, 8; the digits of one operand staged (they fit beside the 80 KB disc state)");
   static constexpr int THREADS = 512;
   static constexpr size_t STATE_BYTES = (size_t)GL::CAP * 16 + (size_t)GL::CAP * 4;
   static constexpr size_t TW_BYTES = sizeof(TwC<double>) * (size_t)G4<M>::S_ENT;

@@ -52,7 +52,7 @@ int v6_launch(int prec, int m, const KParams &kp, int grid, cudaStream_t s);
 // circular containment sets on the one-CTA radix-8 schedule: m = 2^10 .. 2^13 (fp64)
 int d3_info(int m, LaunchInfo *li);
 int d3_launch(int m, const KParams &kp, int grid, cudaStream_t s);
-// ... and on the cluster schedule: m = 2^14, 2^15 (fp64, 16-byte aligned digit rows)
+// ... and on the cluster schedule: m = 2^14 .. 2^16 (fp64, 16-byte aligned digit rows)
 int d4_info(int m, LaunchInfo *li);
 int d4_launch(int m, const KParams &kp, int clusters, cudaStream_t s);
 // m = 2^14 .. 2^16: one thread-block cluster of m/8192 CTAs per multiplication

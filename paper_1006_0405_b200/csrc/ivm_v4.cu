@@ -229,7 +229,7 @@ int v4_launch(int prec, int m, const KParams &kp, int clusters, cudaStream_t s) 
 }
 
 
-// ---- circular containment sets on the cluster schedule (ivm_d4.cuh): fp64, m = 2^14, 2^15 ----
+// ---- circular containment sets on the cluster schedule (ivm_d4.cuh): fp64, m = 2^14 .. 2^16 ----
 template <int M> static void d4_cfg(cudaLaunchConfig_t &cfg, cudaLaunchAttribute *attr, int clusters, cudaStream_t s) {
   using CF = d4::CfgD4<M>;
   constexpr int C = v4::G4<M>::C;
@@ -266,6 +266,7 @@ int d4_info(int m, LaunchInfo *li) {
   switch (m) {
     case 14: return d4_info_m<14>(li);
     case 15: return d4_info_m<15>(li);
+    case 16: return d4_info_m<16>(li);
     default: return -4;
   }
 }
@@ -279,6 +280,7 @@ int d4_launch(int m, const KParams &kp, int clusters, cudaStream_t s) {
   switch (m) {
     case 14: return d4_go<14>(kp, clusters, s);
     case 15: return d4_go<15>(kp, clusters, s);
+    case 16: return d4_go<16>(kp, clusters, s);
     default: return -4;
   }
 }
