@@ -494,7 +494,7 @@ def main():
     ap.add_argument("--gather", action="store_true",
                     help="also time the step with the products gathered to rank 0 (pipelined NCCL sends)")
     ap.add_argument("--gather-chunks", type=int, default=4)
-    ap.add_argument("--other-configs", default="C1,C3,C5,C2-disc",
+    ap.add_argument("--other-configs", default="C1,C3,C5,C2-disc,C3-disc,C5-disc",
                     help="at N = 1 also time these configs (same protocol) into the line's other_configs; '' for none")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
