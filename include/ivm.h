@@ -182,14 +182,14 @@ int ivm_multiply_naive(ivm_ctx_t ctx, const uint8_t *a, const uint8_t *b, size_t
  * not certified); cert: device [batch] (1 = proved exact); max_radius:
  * device [batch] largest disc radius over the 2n-1 used coefficients, or NULL.
  * n <= ivm_max_digits(IVM_F64) (m <= 2^18; IVM_EUNSUPPORTED otherwise).
- * Kernels: for m = 2^10 .. 2^13, and for m >= 2^14 when the digit rows are
- * aligned (a, b and n multiples of 16 bytes for m <= 2^16, of 4 bytes above),
- * the odd-frequency radix-8 schedules of ivm_multiply_batched (one CTA, a
- * thread-block cluster, or pipelined CTA groups per multiplication) with a disc
- * as the element; otherwise the radix-2 DIT (one CTA for m <= 8192, else a
- * group of m/8192 co-resident CTAs, the DIT factored as 8192 x m/8192 through
- * device scratch).  Same results contract either way (certified => exact; the
- * radii differ within a small factor).  Asynchronous on `cuda_stream`; uses
+ * Kernels: for m >= 2^10 the odd-frequency radix-8 schedules of
+ * ivm_multiply_batched (one CTA, a thread-block cluster, or pipelined CTA
+ * groups per multiplication) with a disc as the element (fastest with aligned
+ * digit rows: a, b and n multiples of 16 bytes); below, and everywhere under
+ * IVM_DISC3=0, the radix-2 DIT (one CTA for m <= 8192, else a group of m/8192
+ * co-resident CTAs, the DIT factored as 8192 x m/8192 through device scratch).
+ * Same results contract either way (certified => exact; the radii differ
+ * within a small factor).  Asynchronous on `cuda_stream`; uses
  * context-owned device scratch. */
 int ivm_multiply_disc(ivm_ctx_t ctx, const uint8_t *a, const uint8_t *b, size_t n, size_t batch,
                       uint8_t *prod, uint8_t *cert, double *max_radius, void *cuda_stream);

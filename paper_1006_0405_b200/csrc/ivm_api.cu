@@ -1049,10 +1049,9 @@ int ivm_multiply_disc(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, size_t n,
     c->last_launches = 1;
     return IVM_OK;
   }
-  if (lg >= 14 && lg <= 16 && c->disc3 && n % 16 == 0 &&
-      ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) % 16) == 0) {
+  if (lg >= 14 && lg <= 16 && c->disc3) {
     // the cluster schedule in disc arithmetic (ivm_d4.cuh), on the rectangular cluster
-    // kernel's tables; unaligned rows keep the radix-2 group kernel below
+    // kernel's tables (IVM_DISC3=0: the radix-2 group kernel below)
     const void *tw4;
     ivm::LaunchInfo li;
     int r = get_table4(c, lg, IVM_F64, &tw4);
@@ -1076,10 +1075,9 @@ int ivm_multiply_disc(ivm_ctx_t c, const uint8_t *a, const uint8_t *b, size_t n,
     c->last_launches = 1;
     return IVM_OK;
   }
-  if ((lg == 17 || lg == 18) && c->disc3 && n % 4 == 0 &&
-      ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) % 4) == 0) {
+  if ((lg == 17 || lg == 18) && c->disc3) {
     // the pipelined group schedule in disc arithmetic (ivm_d7.cuh), on the rectangular
-    // kernel's tables and scratch layout; unaligned rows keep the radix-2 group kernel below
+    // kernel's tables and scratch layout (IVM_DISC3=0: the radix-2 group kernel below)
     const void *tw4;
     ivm::LaunchInfo li;
     int r = get_table4(c, lg, IVM_F64, &tw4);

@@ -1,7 +1,7 @@
 // ivm_d4.cuh -- circular containment sets (R15) on the cluster
 // schedule of ivm_v4.cuh: fp64, m = 2^14 .. 2^16, one thread-block cluster of
-// C = m/8192 CTAs per multiplication, digits staged by bulk copies (16-byte
-// aligned rows; the host falls back to the radix-2 group kernel otherwise).
+// C = m/8192 CTAs per multiplication, digits staged by bulk copies when every row
+// is 16-byte aligned, else read through L2.
 // Included by ivm_v4.cu after ivm_v4.cuh and ivm_d3.cuh.
 //
 // Same row split, role tables, passes, exchanges, certificate and carry as
@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(512, 1) ivm_d4_kernel(KParams kp) {
     mbar_init(&dbar);
   }
   __syncthreads();
+  const bool staged = n % 16 == 0 && ((reinterpret_cast<uintptr_t>(kp.a) | reinterpret_cast<uintptr_t>(kp.b)) % 16) == 0;
   if (threadIdx.x == 0 && cid < kp.batch) {
     mbar_expect(&tbar, EB * (X::FLAST + X::MF_ENT + X::MI_ENT + 2 * C + 16 * C));
     bulk_copy(twb + X::S_SWAP, tw + X::FWD(crank) + X::FP(4), EB * X::FLAST, &tbar);
@@ -76,8 +77,10 @@ __global__ void __launch_bounds__(512, 1) ivm_d4_kernel(KParams kp) {
     bulk_copy(twb + X::S_MI, tw + X::INV, EB * X::MI_ENT, &tbar);
     bulk_copy(twb + X::S_TH, tw + X::TH(crank), EB * 2 * C, &tbar);
     bulk_copy(twb + X::S_TH1, tw + X::TH1(crank), EB * 16 * C, &tbar);
-    mbar_expect(&dbar, (unsigned)n);  // operand a of the first pair (dbar phases: a = even, b = odd)
-    bulk_copy(sdig, kp.a + (size_t)cid * n, (unsigned)n, &dbar);
+    if (staged) {
+      mbar_expect(&dbar, (unsigned)n);  // operand a of the first pair (dbar phases: a = even, b = odd)
+      bulk_copy(sdig, kp.a + (size_t)cid * n, (unsigned)n, &dbar);
+    }
   }
   if (cid < kp.batch) mbar_wait(&tbar, 0);
   // tbar phases per pair it: 3 it (forward-last), 3 it + 1 (inverse pass 3), 3 it + 2 (last inverse pass)
@@ -85,9 +88,17 @@ __global__ void __launch_bounds__(512, 1) ivm_d4_kernel(KParams kp) {
   int it = 0;
   for (int pair = cid; pair < kp.batch; pair += ncl, it++) {
     const unsigned par = (unsigned)it & 1u;
+    if (!staged && pair + ncl < kp.batch) {  // L2 prefetch of the next pair's digits
+      const int nxt = pair + ncl;
+      for (int off = (int)threadIdx.x * 128; off < n; off += (int)blockDim.x * 128) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(kp.a + (size_t)nxt * n + off));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(kp.b + (size_t)nxt * n + off));
+      }
+    }
 #pragma unroll 1
     for (int op = 0; op < 2; op++) {
-      mbar_wait(&dbar, (unsigned)op);
+      if (staged) mbar_wait(&dbar, (unsigned)op);
+      const uint8_t *dsrc = staged ? sdig : (op == 0 ? kp.a : kp.b) + (size_t)pair * n;
       {  // the cross pass fused with local pass 1 (cross_pass1), stored in the pass-2 layout
         const PassRT pp = pick_fwd4<M>(0);
         // TH1: [8 j][C q] full intervals (rl, rh, il, ih); the lower corner is the center
@@ -101,7 +112,7 @@ __global__ void __launch_bounds__(512, 1) ivm_d4_kernel(KParams kp) {
           for (int q = 0; q < C; q++) {
             const double4 th = th1[j * C + q];
             const int idx = t + 512 * j + 4096 * q;
-            const unsigned d = idx < n ? (unsigned)sdig[idx] : 0u;
+            const unsigned d = idx < n ? (unsigned)dsrc[idx] : 0u;
             const double x = digit_val<double>(d);
             s1 += d;
             cr = __fma_rn(x, th.x, cr);
@@ -128,7 +139,7 @@ __global__ void __launch_bounds__(512, 1) ivm_d4_kernel(KParams kp) {
         cs.maxrad = 0ull;
       }
       __syncthreads();
-      if (threadIdx.x == 0) {  // the next operand: b of this pair, or a of the next
+      if (staged && threadIdx.x == 0) {  // the next operand: b of this pair, or a of the next
         const uint8_t *nx = op == 0 ? kp.b + (size_t)pair * n : kp.a + (size_t)(pair + ncl) * n;
         if (op == 0 || pair + ncl < kp.batch) {
           mbar_expect(&dbar, (unsigned)n);

@@ -1,7 +1,6 @@
 // ivm_d7.cuh -- circular containment sets (R15) on the pipelined
 // group schedule of ivm_v7.cuh: fp64, m = 2^17, 2^18 (C = 16, 32 tasks per
-// multiplication), word-aligned digit rows (the host falls back to the radix-2
-// group kernel otherwise).  Included by ivm_v5.cu after ivm_v7.cuh and ivm_d3.cuh.
+// multiplication).  Included by ivm_v5.cu after ivm_v7.cuh and ivm_d3.cuh.
 //
 // Same task split, stages (L / A / Cs), counters, ring, tables, certificate and
 // carry as ivm_v7_kernel; the element is a disc (arithmetic: ivm_d3.cuh).  The
@@ -43,7 +42,7 @@ __device__ __forceinline__ DI ldcg_xd(const XD *p) {
 }
 
 // the tensor-core cross pass (cross_tc of ivm_v5.cuh, word loads) with disc outputs
-template <int M>
+template <int M, bool WORDS>
 __device__ __forceinline__ void cross_tc_d(const uint8_t *__restrict__ dig, int n, BufD st, const void *limbs,
                                            unsigned crank) {
   constexpr int C = G4<M>::C;
@@ -54,14 +53,14 @@ __device__ __forceinline__ void cross_tc_d(const uint8_t *__restrict__ dig, int 
   const bool rowhi = t >= 2, im = (t & 1) != 0;
   double *cpl = reinterpret_cast<double *>(st.c);
   unsigned nx[4][4];
-  tc_load_group<C, true>(dig, n, warp * 256, g, t, nx);
+  tc_load_group<C, WORDS>(dig, n, warp * 256, g, t, nx);
 #pragma unroll 1
   for (int grp = 0; grp < 4; grp++) {
     const int vb = warp * 256 + grp * 64;
     unsigned a[4][4];
 #pragma unroll
     for (int r = 0; r < 4; r++) tr4x4(nx[r][0], nx[r][1], nx[r][2], nx[r][3], a[r]);
-    if (grp < 3) tc_load_group<C, true>(dig, n, vb + 64, g, t, nx);
+    if (grp < 3) tc_load_group<C, WORDS>(dig, n, vb + 64, g, t, nx);
 #pragma unroll
     for (int j = 0; j < 4; j++) {
       int x[4][2];
@@ -151,7 +150,11 @@ __global__ void __launch_bounds__(512, 1) ivm_d7_kernel(KParams kp, Pipe7 g) {
       }
 #pragma unroll 1
       for (int op = 0; op < 2; op++) {
-        cross_tc_d<M>((op == 0 ? kp.a : kp.b) + (size_t)pair * n, n, st, tw + X::LIMB, role);
+        {  // word loads when every row is word-aligned, else byte loads
+          const uint8_t *dg = (op == 0 ? kp.a : kp.b) + (size_t)pair * n;
+          if (((reinterpret_cast<uintptr_t>(dg) | (uintptr_t)n) & 3) == 0) cross_tc_d<M, true>(dg, n, st, tw + X::LIMB, role);
+          else cross_tc_d<M, false>(dg, n, st, tw + X::LIMB, role);
+        }
         __syncthreads();
         IVM_PH(2 * op);
 #pragma unroll  // (specialised per pass: addresses fold into immediates)

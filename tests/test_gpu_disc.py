@@ -77,9 +77,9 @@ def test_disc_rejects_too_large(ctx):
 
 @pytest.mark.parametrize("n", [4097, 4112, 5000, 6000, 8192, 8193, 8208, 12000, 16384, 20000, 40000])
 def test_disc_group_parity_with_oracle(ctx, n):
-    """m = 2^14 .. 2^17: the cluster kernel in disc arithmetic (m = 2^14 .. 2^16,
-    n a multiple of 16: ivm_d4.cuh), the pipelined group kernel (m = 2^17, n a
-    multiple of 4: ivm_d7.cuh) and the radix-2 group kernel (8192 x m/8192
+    """m = 2^14 .. 2^17: the cluster kernel in disc arithmetic (m = 2^14 .. 2^16:
+    ivm_d4.cuh) and the pipelined group kernel (m = 2^17: ivm_d7.cuh), aligned and
+    unaligned digit rows (8192 x m/8192
     DIT factorization; the other sizes) against the disc oracle: products bit-exact, flags where the oracle
     certifies with margin, radius within 2x (and not below 1/4)."""
     K = inputs.KINDS
@@ -155,11 +155,12 @@ def test_disc_radix8_kernel_against_radix2_kernel(n, monkeypatch):
     print("radix-8 / radix-2 disc radius", n, ratio.min(), ratio.max())
 
 
-@pytest.mark.parametrize("n,B", [(8192, 230), (16384, 120), (20000, 70), (32768, 50), (40000, 40), (65536, 24), (75000, 20), (131072, 10)])
+@pytest.mark.parametrize("n,B", [(8192, 230), (9001, 90), (16384, 120), (20000, 70), (32768, 50), (40000, 40), (50001, 30), (65536, 24), (75000, 20), (131072, 10)])
 def test_disc_cluster_kernel_against_group_kernel(n, B, monkeypatch):
-    """m = 2^14 .. 2^16 with 16-byte aligned rows run the cluster schedule in disc
-    arithmetic (csrc/ivm_d4.cuh), m = 2^17, 2^18 with word-aligned rows the pipelined
-    group schedule (csrc/ivm_d7.cuh); IVM_DISC3=0 keeps the radix-2 group kernel.  A
+    """m = 2^14 .. 2^16 run the cluster schedule in disc arithmetic (csrc/ivm_d4.cuh;
+    staged digits for 16-byte aligned rows, else through L2: n = 9,001), m = 2^17, 2^18
+    the pipelined group schedule (csrc/ivm_d7.cuh; word or byte digit loads: n = 50,001);
+    IVM_DISC3=0 keeps the radix-2 group kernel.  A
     batch of several pairs per cluster / several tasks per CTA, all digit kinds: same products and flags,
     radii within 2x of each other, a sample bit-exact against Python ints."""
     import torch
