@@ -116,8 +116,9 @@ __device__ __forceinline__ DI dctw(const DI &o, int j, int M) {
 }
 
 // radix-8 DIT in dit8's order (ivm_v3.cuh)
-template <bool INV, typename IN>
-__device__ __forceinline__ void ddit8(DI (&v)[8], IN &&in) {
+struct NoOp { __device__ __forceinline__ void operator()() const {} };
+template <bool INV, typename IN, typename AL = NoOp>
+__device__ __forceinline__ void ddit8(DI (&v)[8], IN &&in, AL &&loaded = AL()) {
   DI a0 = in(0), a1 = in(4);
   dbfly(a0, a1, DI(a1));
   DI a2 = in(2), a3 = in(6);
@@ -127,6 +128,7 @@ __device__ __forceinline__ void ddit8(DI (&v)[8], IN &&in) {
   DI a4 = in(1), a5 = in(5);
   dbfly(a4, a5, DI(a5));
   DI a6 = in(3), a7 = in(7);
+  loaded();  // every input has been read
   dbfly(a6, a7, DI(a7));
   dbfly(a4, a6, DI(a6));
   dbfly(a5, a7, dctw<INV>(a7, 1, 4));
@@ -193,7 +195,13 @@ __global__ void __launch_bounds__(CfgD<M>::THREADS, CfgD<M>::MINB) ivm_d3_kernel
   constexpr int N = C::N, R = 8;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Cert3 cs;
-  __shared__ __align__(8) unsigned long long tbar;
+  __shared__ __align__(8) unsigned long long tbar, pbar;
+#ifndef IVM_D3_NOSPLIT
+  unsigned long long *wbar = &pbar;  // split write-after-read barrier of the mid passes (ivm_v3.cuh)
+#else
+  unsigned long long *wbar = nullptr;
+#endif
+  unsigned pph = 0u;
   BufD st{reinterpret_cast<double2 *>(smem), reinterpret_cast<float *>(smem + (size_t)C::CAP * 16)};
   int32_t *coef = reinterpret_cast<int32_t *>(smem);
   TwC<double> *twb = reinterpret_cast<TwC<double> *>(smem + C::STATE_BYTES);
@@ -211,7 +219,11 @@ __global__ void __launch_bounds__(CfgD<M>::THREADS, CfgD<M>::MINB) ivm_d3_kernel
   constexpr int QS = C::THREADS;
   constexpr double SCALE = 2.0 / (double)N;  // |omega| of the last pass's tables
 
-  if (threadIdx.x == 0) mbar_init(&tbar);
+  if (threadIdx.x == 0) {
+    mbar_init(&tbar);
+    const unsigned pa = (unsigned)__cvta_generic_to_shared(&pbar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(pa), "r"((unsigned)(C::THREADS / 32)));
+  }
   __syncthreads();
   if (threadIdx.x == 0 && blockIdx.x < kp.batch) {
     mbar_expect(&tbar, FL_BYTES + SMF_BYTES + SMI_BYTES);
@@ -281,9 +293,16 @@ __global__ void __launch_bounds__(CfgD<M>::THREADS, CfgD<M>::MINB) ivm_d3_kernel
           if (q == 0) return z;
           const TwC<double> w = tp[(q - 1) * tstride];
           return (2 * q <= R) ? drt<false, false>(w, z) : drt<false, true>(w, z);
+        }, [&]() {
+          if (wbar && i < NFWD - 1) pb_arrive_warp(wbar);
         });
         if (i < NFWD - 1) {
-          __syncthreads();
+          if (wbar) {
+            mbar_wait(wbar, pph);
+            pph ^= 1u;
+          } else {
+            __syncthreads();
+          }
 #pragma unroll
           for (int r = 0; r < R; r++) {
             if (2 * r < R) st.st(sidx(k0 + pp.L * r, nu, pp.RSo, pp.SWo), v[r]);
@@ -338,8 +357,16 @@ __global__ void __launch_bounds__(CfgD<M>::THREADS, CfgD<M>::MINB) ivm_d3_kernel
         const TwC<double> w = tp[q * pp.L];
         if (last) return drt<false, true, true>(w, d, SCALE);
         return (4 * qq > R) ? drt<false, true>(w, d) : drt<false, false>(w, d);
+      }, [&]() {
+        if (wbar && !last) pb_arrive_warp(wbar);
       });
-      __syncthreads();  // every input loaded (last pass: the coefficients may overwrite the state)
+      // every input loaded (last pass: the coefficients may overwrite the state)
+      if (wbar && !last) {
+        mbar_wait(wbar, pph);
+        pph ^= 1u;
+      } else {
+        __syncthreads();
+      }
       if (last) {
 #pragma unroll
         for (int r = 0; r < R; r++) {
