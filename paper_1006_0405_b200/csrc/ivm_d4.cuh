@@ -7,10 +7,10 @@
 // Same row split, role tables, passes, exchanges, certificate and carry as
 // ivm_v4_kernel; the element is a disc (arithmetic: ivm_d3.cuh).  The cross pass
 // fused with local pass 1 (cross_pass1) sums x_q Theta[j][q] over the C digit
-// terms of input j: the center by a chain of round-to-nearest FMAs (every
-// partial sum has |re|, |im| <= S1 = sum_q x_q, so the C roundings cost at most
-// C U S1 in modulus), the table centers are within RW of the true roots of unity
-// (another RW S1): r = S1 (RW + C U) rounded up.
+// terms of input j: the center by a chain of round-to-nearest FMAs (partial sum k
+// has |re|, |im| <= S1_k = sum_{q<=k} x_q, so the roundings cost at most
+// U sum_k S1_k in modulus), the table centers are within RW of the true roots of
+// unity (another RW S1): r = RW S1 + U sum_k S1_k, rounded up.
 #pragma once
 
 namespace ivm {
@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(512, 1) ivm_d4_kernel(KParams kp) {
         DI v[R];
         ddit8<false>(v, [&](int j) {
           double cr = 0.0, ci = 0.0;
-          unsigned s1 = 0u;
+          unsigned s1 = 0u, ss = 0u;  // S1 and the sum of its partial sums S1_k
 #pragma unroll
           for (int q = 0; q < C; q++) {
             const double4 th = th1[j * C + q];
@@ -115,11 +115,12 @@ __global__ void __launch_bounds__(512, 1) ivm_d4_kernel(KParams kp) {
             const unsigned d = idx < n ? (unsigned)dsrc[idx] : 0u;
             const double x = digit_val<double>(d);
             s1 += d;
+            ss += s1;
             cr = __fma_rn(x, th.x, cr);
             ci = __fma_rn(x, th.z, ci);
           }
-          // (RW + C U) S1, rounded up (S1 < 2^13 exact)
-          return DI{cr, ci, __dmul_ru((double)s1, (DRW + C * DU) * (1.0 + 0x1p-40))};
+          // RW S1 + U sum_k S1_k (partial sum k is bounded by S1_k per part), rounded up
+          return DI{cr, ci, __dmul_ru(__fma_ru((double)ss, DU, __dmul_ru((double)s1, DRW)), 1.0 + 0x1p-40)};
         });
         if (op == 0 && it > 0) cluster_wait();  // the previous pair's remote reads of this state are done
         const int nu = t;
